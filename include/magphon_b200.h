@@ -1,0 +1,167 @@
+/*
+ * magphon_b200.h -- C ABI of the B200 coupled Maxwell-LLG stepper.
+ *
+ * This is the drop-in boundary for the hot loop of the reference solver,
+ * ``magphon.sim.run`` (reference pkg/src/magphon/sim.py:151-171): one call
+ * advances the lattice through whole coupled steps (curl E -> H / LLG fixed
+ * point -> curl H -> semi-implicit E -> walls -> soft source -> probes).
+ * The reference has no FFI of its own (it is pure numpy); each entry point
+ * below names the reference function(s) whose work it takes over.  The
+ * Python host mirror (paper_2510_22221_b200/_native.py) binds it with
+ * ctypes; INTEGRATION.md shows the binding a magphon maintainer would add.
+ *
+ * Conventions
+ *  - Plain C types only; no torch / CUDA types in signatures.  Host arrays
+ *    are C-order float64 in the reference allocation layout (grid.py:82-99):
+ *    each E/H component has field_shape = (n+1 on active axes, 1 on
+ *    collapsed ones); M is (3, nx, ny, nz).
+ *  - Every function returns MPB_OK (0) or an error code; the message of the
+ *    last error on the calling thread is available from mpb_last_error().
+ *  - A handle owns all of its device memory and streams; it is not
+ *    thread-safe.  Do not fork after mpb_create.
+ *  - Arithmetic is IEEE fp64 without FMA contraction, in the reference's
+ *    operation order, so results are bit-identical to the reference CPU path.
+ */
+#ifndef MAGPHON_B200_H
+#define MAGPHON_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define MPB_API __attribute__((visibility("default")))
+#else
+#define MPB_API
+#endif
+
+#define MPB_OK 0
+#define MPB_EINVAL 1        /* invalid argument      -> ValueError          */
+#define MPB_ESTEP 2         /* LLG fixed point failed -> llg.StepFailure    */
+#define MPB_ECUDA 3         /* CUDA / NCCL error      -> RuntimeError       */
+
+#define MPB_FACE_PEC 0
+#define MPB_FACE_PMC 1
+#define MPB_FACE_MUR1 2
+
+#define MPB_MAX_MATERIALS 256
+#define MPB_MAX_ITERS_CAP 1000
+
+/* Probe / field component codes: Ex Ey Ez Hx Hy Hz Mx My Mz. */
+#define MPB_COMP_EX 0
+#define MPB_COMP_HX 3
+#define MPB_COMP_MX 6
+
+/* One entry of the material table.  Every coefficient is precomputed on the
+ * host with the reference's own numpy expressions so the device only ever
+ * multiplies/adds/divides them in the reference order:
+ *   ca, cb      em.py:239-254   (1/(sigma/2+eps/dt), sigma/2-eps/dt)
+ *   mur_k[a]    em.py:352-357   ((c dt - d_a)/(c dt + d_a), c = 1/sqrt(mu0 eps))
+ *   c_llg       llg.py:125      (mu0*|gamma|*dt/2)
+ *   alpha_ms    llg.py:132      (alpha/Ms)                                  */
+typedef struct mpb_material {
+    double ca, cb;
+    double mur_k[3];
+    double Ms;
+    double alpha_ms;
+    double c_llg;
+    double hbias[3];
+    int32_t magnetic;       /* Ms > 0 */
+    int32_t pad_;
+} mpb_material;
+
+typedef struct mpb_setup {
+    int32_t n[3];           /* cell counts nx, ny, nz (grid.py:41-74)        */
+    double d[3];            /* spacings dx, dy, dz                            */
+    double dt;              /* SimConfig.dt  (sim.py:52-54)                   */
+    double coef_h;          /* dt/mu0        (em.py:178, llg.py:105)          */
+    int32_t faces[6];       /* x0 x1 y0 y1 z0 z1, MPB_FACE_*                  */
+    int32_t n_materials;
+    const mpb_material* materials;
+    const uint8_t* cell_material;   /* (nx,ny,nz) C-order material ids        */
+    int32_t src_loc[3];     /* already wrapped into range by the caller       */
+    double src_pol[3];      /* SourceSpec.polarization                        */
+    int32_t n_probes;
+    const int32_t* probe_comp;      /* n_probes codes                         */
+    const int32_t* probe_loc;       /* 3*n_probes indices                     */
+    double llg_tol;         /* LlgIterationParams (llg.py:49-58)             */
+    int32_t llg_max_iters;
+    int32_t device;         /* CUDA ordinal                                   */
+    int32_t kernel_variant; /* 0 = default (fused sweep), 1 = split H/E sweeps */
+    int32_t graph_steps;    /* steps per captured CUDA graph (0 = default)    */
+} mpb_setup;
+
+/* Failure record of an LLG step (llg.py:139-148 + sim.py:161-164). */
+typedef struct mpb_failure {
+    int64_t step;           /* -1 if no failure                                */
+    double residual;
+    int32_t iterations;
+    int32_t kind;           /* 1 = diverging, 2 = budget exhausted            */
+} mpb_failure;
+
+typedef struct mpb_handle mpb_handle;
+
+/* Library / build identification, e.g. "magphon_b200 0.1 sm_100a fmad=false". */
+MPB_API const char* mpb_version(void);
+
+/* Message of the last error on this thread ("" if none). */
+MPB_API const char* mpb_last_error(void);
+
+/* Allocate device state for one run and upload the material table.
+ * Replaces: grid.allocate + _MagneticCells + em._e_coefficients /
+ * _nonmagnetic_H_masks setup (grid.py:140-156, sim.py:100-111,
+ * em.py:152-168, em.py:239-254).  Fields start at zero; call
+ * mpb_load_state to set E, H, M (the host computes the initial M). */
+MPB_API int mpb_create(const mpb_setup* setup, mpb_handle** out);
+
+MPB_API void mpb_destroy(mpb_handle* h);
+
+/* Upload / download the full state in reference layout
+ * (FieldLattice.load_state / state_arrays, grid.py:125-137).
+ * fields[0..5] = Ex Ey Ez Hx Hy Hz, each prod(field_shape) doubles;
+ * m = 3*nx*ny*nz doubles. */
+MPB_API int mpb_load_state(mpb_handle* h, const double* const fields[6], const double* m);
+MPB_API int mpb_save_state(mpb_handle* h, double* const fields[6], double* m);
+
+/* Advance nsteps coupled steps.  Replaces the body of sim.run's time loop
+ * (sim.py:151-171).  Host buffers:
+ *   src_vals[s]            source value v((n0+s+1) dt) (em.py:96-101, host)
+ *   probe_out[s*n_probes+p] probe p after step n0+s (sim.py:170-171)
+ *   iters_out[s]           LLG iterations r* of step n0+s (sim.py:167)
+ * On an LLG failure returns MPB_ESTEP and fills *fail (step = n0+s);
+ * probe/iteration rows after the failing step are unspecified. */
+MPB_API int mpb_run(mpb_handle* h, int64_t n0, int64_t nsteps, const double* src_vals,
+            double* probe_out, int32_t* iters_out, mpb_failure* fail);
+
+/* Device-resident variant for benchmarking / chained pipelines: all three
+ * buffers are DEVICE pointers on the handle's device, the work is enqueued
+ * on `stream` (a cudaStream_t, 0 = the handle's own stream) and the call
+ * returns without synchronising.  Check failures with mpb_check_failure. */
+MPB_API int mpb_run_device(mpb_handle* h, int64_t n0, int64_t nsteps,
+                   const double* d_src_vals, double* d_probe_out,
+                   int32_t* d_iters_out, void* stream);
+
+/* Synchronise and report the first LLG failure since the last call. */
+MPB_API int mpb_check_failure(mpb_handle* h, mpb_failure* fail);
+
+/* Per-kernel device timing of the main sweep kernel(s): when enabled, each
+ * launch of the dominant kernel is bracketed by CUDA events on the stream it
+ * runs on (graphs are bypassed).  mpb_kernel_time returns the summed
+ * milliseconds and launch count since enabling, and the name of the kernel. */
+MPB_API int mpb_set_kernel_timing(mpb_handle* h, int enable);
+MPB_API int mpb_kernel_time(mpb_handle* h, double* ms_total, int64_t* launches,
+                    const char** kernel_name);
+
+/* Number of kernel launches the last mpb_run / mpb_run_device enqueued. */
+MPB_API int64_t mpb_launch_count(mpb_handle* h);
+
+/* Device bytes held by the handle. */
+MPB_API int64_t mpb_device_bytes(mpb_handle* h);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MAGPHON_B200_H */

@@ -1,0 +1,350 @@
+// mpb_kernels_split.cuh -- per-step kernels shared by both sweep variants
+// (LLG fixup, walls, source+probes) and the split H / E sweeps.
+#pragma once
+
+#include <cooperative_groups.h>
+
+#include "mpb_device.cuh"
+
+namespace mpb {
+
+namespace cg = cooperative_groups;
+
+// ---------------------------------------------------------------------------
+// Per-CTA LLG statistics: residual history and local stop range, reduced in
+// shared memory and flushed with one global atomic per iterate per CTA.
+// ---------------------------------------------------------------------------
+struct CtaLlgStats {
+    unsigned long long* hist;   // dynamic smem, max_iters + 2 entries
+    int* rc;                    // [0] = min, [1] = max
+};
+
+__device__ __forceinline__ void cta_stats_init(CtaLlgStats& s, int max_iters) {
+    for (int r = threadIdx.x; r <= max_iters + 1; r += blockDim.x) s.hist[r] = 0ull;
+    if (threadIdx.x == 0) { s.rc[0] = 0x7fffffff; s.rc[1] = 0; }
+}
+
+__device__ __forceinline__ void cta_stats_flush(const CtaLlgStats& s, int max_iters,
+                                                StepState* st) {
+    for (int r = 1 + threadIdx.x; r <= max_iters; r += blockDim.x) {
+        const unsigned long long v = s.hist[r];
+        if (v) atomicMax(&st->hist[r], v);
+    }
+    if (threadIdx.x == 0) {
+        atomicMin(&st->rc_min, s.rc[0]);
+        atomicMax(&st->rc_max, s.rc[1]);
+    }
+}
+
+// Run one magnetic cell to its local stop: the first iterate whose own
+// residual is <= tol, or max_iters.  Because cells couple only through the
+// global stop test, the iterate sequence of a cell is the same as in the
+// reference's lockstep loop; the global r* is settled afterwards
+// (k_llg_fixup).  Returns the local stop index (max_iters+1 if none).
+__device__ __forceinline__ int llg_local(LlgCell& s, const Geom& g, double Hr[3],
+                                         double Mr[3], CtaLlgStats& cs) {
+    Hr[0] = s.Hn[0]; Hr[1] = s.Hn[1]; Hr[2] = s.Hn[2];
+    Mr[0] = s.Mn[0]; Mr[1] = s.Mn[1]; Mr[2] = s.Mn[2];
+    for (int r = 1; r <= g.max_iters; ++r) {
+        const double res = llg_iterate(s, g.coef_h, Hr, Mr);
+        atomicMax(&cs.hist[r], dbits(res));
+        if (res <= g.tol) return r;
+    }
+    return g.max_iters + 1;
+}
+
+// ---------------------------------------------------------------------------
+// Split variant, kernel 1: H^{n+1} everywhere (em.py:171-182 plus the local
+// part of llg.coupled_cell_step).  One thread per allocation entry (i, f).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_hsweep(Geom g, Bufs b,
+                                                const mpb_material* __restrict__ mats,
+                                                const uint8_t* __restrict__ ids,
+                                                StepState* st) {
+    extern __shared__ unsigned long long smem_hist[];
+    __shared__ int smem_rc[2];
+    if (st->fail) return;
+    const int i = blockIdx.y;
+    const int f = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool live = f < g.FyFz;
+    int j = 0, k = 0;
+    if (live) { j = f / g.F[2]; k = f - j * g.F[2]; }
+    const int64_t o = i * g.PP + f;
+    const bool cellin = live && i < g.n[0] && j < g.n[1] && k < g.n[2];
+    const bool magnetic = cellin && mats[ids[o]].magnetic;
+    const int anymag = __syncthreads_or(magnetic);
+    CtaLlgStats cs{smem_hist, smem_rc};
+    if (anymag) { cta_stats_init(cs, g.max_iters); __syncthreads(); }
+    if (live) {
+        const bool vx = j < g.n[1] && k < g.n[2];
+        const bool vy = i < g.n[0] && k < g.n[2];
+        const bool vz = i < g.n[0] && j < g.n[1];
+        const Curl3 c = curl_e_at(g, b.Ea, o, g.PP, g.F[2], vx, vy, vz);
+        if (!magnetic) {
+            if (vx) b.Hb[0][o] = b.Ha[0][o] - g.coef_h * c.x;
+            if (vy) b.Hb[1][o] = b.Ha[1][o] - g.coef_h * c.y;
+            if (vz) b.Hb[2][o] = b.Ha[2][o] - g.coef_h * c.z;
+        } else {
+            const mpb_material m = mats[ids[o]];
+            const int64_t om = (int64_t)(i - g.mx0) * g.PP + f;
+            LlgCell s;
+            s.Hn[0] = b.Ha[0][o]; s.Hn[1] = b.Ha[1][o]; s.Hn[2] = b.Ha[2][o];
+            s.Mn[0] = b.Ma[0][om]; s.Mn[1] = b.Ma[1][om]; s.Mn[2] = b.Ma[2][om];
+            s.cE[0] = c.x; s.cE[1] = c.y; s.cE[2] = c.z;
+            llg_setup(s, m);
+            double Hr[3], Mr[3];
+            const int rc = llg_local(s, g, Hr, Mr, cs);
+            atomicMin(&cs.rc[0], rc);
+            atomicMax(&cs.rc[1], rc);
+            b.Hb[0][o] = Hr[0]; b.Hb[1][o] = Hr[1]; b.Hb[2][o] = Hr[2];
+            b.Mb[0][om] = Mr[0]; b.Mb[1][om] = Mr[1]; b.Mb[2][om] = Mr[2];
+        }
+    }
+    if (anymag) { __syncthreads(); cta_stats_flush(cs, g.max_iters, st); }
+}
+
+// ---------------------------------------------------------------------------
+// Split variant, kernel 2: E^{n+1} = ca (curl H - cb E) on every allocation
+// entry (em.py:206-232, 257-272).  Walls are applied afterwards.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void e_update_at(const Geom& g, const Bufs& b,
+                                            const mpb_material* __restrict__ mats,
+                                            const uint8_t* __restrict__ ids, int i,
+                                            int j, int k, int64_t o) {
+    const double* const* H = b.Hb;
+    double cx = 0.0, cy = 0.0, cz = 0.0;
+    const int64_t sx = g.PP, sy = g.F[2];
+    const bool p[6] = {g.faces[0] == MPB_FACE_PMC, g.faces[1] == MPB_FACE_PMC,
+                       g.faces[2] == MPB_FACE_PMC, g.faces[3] == MPB_FACE_PMC,
+                       g.faces[4] == MPB_FACE_PMC, g.faces[5] == MPB_FACE_PMC};
+    if (g.act[1]) {   // cHx += dHz/dy ; cHz -= dHx/dy
+        cx = cx + bwd_diff(H[2], o, sy, j, g.n[1], g.d[1], p[2], p[3]);
+        cz = cz - bwd_diff(H[0], o, sy, j, g.n[1], g.d[1], p[2], p[3]);
+    }
+    if (g.act[2]) {   // cHx -= dHy/dz ; cHy += dHx/dz
+        cx = cx - bwd_diff(H[1], o, 1, k, g.n[2], g.d[2], p[4], p[5]);
+        cy = cy + bwd_diff(H[0], o, 1, k, g.n[2], g.d[2], p[4], p[5]);
+    }
+    if (g.act[0]) {   // cHy -= dHz/dx ; cHz += dHy/dx
+        cy = cy - bwd_diff(H[2], o, sx, i, g.n[0], g.d[0], p[0], p[1]);
+        cz = cz + bwd_diff(H[1], o, sx, i, g.n[0], g.d[0], p[0], p[1]);
+    }
+    const uint8_t id = ids[o];
+    const double ca = mats[id].ca, cb = mats[id].cb;
+    b.Eb[0][o] = ca * (cx - cb * b.Ea[0][o]);
+    b.Eb[1][o] = ca * (cy - cb * b.Ea[1][o]);
+    b.Eb[2][o] = ca * (cz - cb * b.Ea[2][o]);
+}
+
+__global__ void __launch_bounds__(256) k_esweep(Geom g, Bufs b,
+                                                const mpb_material* __restrict__ mats,
+                                                const uint8_t* __restrict__ ids,
+                                                const StepState* st) {
+    if (st->fail) return;
+    const int i = blockIdx.y;
+    const int f = blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= g.FyFz) return;
+    const int j = f / g.F[2];
+    const int k = f - j * g.F[2];
+    e_update_at(g, b, mats, ids, i, j, k, i * g.PP + f);
+}
+
+// ---------------------------------------------------------------------------
+// LLG fixup: settles r* for the step (llg.py:131-148).
+//  * uniform case -- every magnetic cell stopped locally at the same iterate
+//    R <= max_iters: the sweep's results are final; replay the stop/failure
+//    rule on the complete residual history.
+//  * otherwise: recompute all magnetic cells in lockstep exactly as the
+//    reference does (one grid barrier per iterate) and overwrite H, M.
+// Cooperative launch; every block takes the same branch.
+// ---------------------------------------------------------------------------
+struct MagScratch {    // per magnetic cell, structure of arrays
+    double* v;         // 12 * nmag: Hn[3] Mn[3] cE[3] Mr[3]
+};
+
+__global__ void __launch_bounds__(256) k_llg_fixup(Geom g, Bufs b,
+                                                   const mpb_material* __restrict__ mats,
+                                                   const uint8_t* __restrict__ ids,
+                                                   const int2* __restrict__ cells, int nmag,
+                                                   MagScratch scr, StepState* st) {
+    __shared__ unsigned long long red[32];
+    if (st->fail) return;
+    const int rmin = st->rc_min, rmax = st->rc_max;
+    if (rmin == rmax && rmax <= g.max_iters) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            double fr; int fi, fk;
+            const int r = llg_decide(st->hist, rmax, g.max_iters, g.tol, &fr, &fi, &fk);
+            if (r > 0) {
+                st->rstar = r;
+            } else {   // r == -1 is impossible here: hist[rmax] <= tol
+                st->fail = 1; st->fail_step = st->step; st->fail_res = fr;
+                st->fail_it = fi; st->fail_kind = fk;
+            }
+        }
+        return;
+    }
+    cg::grid_group grid = cg::this_grid();
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int nth = gridDim.x * blockDim.x;
+    double* v = scr.v;
+    // gather Hn, Mn, curl E (from the untouched read buffers)
+    for (int q = tid; q < nmag; q += nth) {
+        const int i = cells[q].x, f = cells[q].y;
+        const int j = f / g.F[2], k = f - j * g.F[2];
+        (void)k;
+        const int64_t o = i * g.PP + f;
+        const int64_t om = (int64_t)(i - g.mx0) * g.PP + f;
+        const Curl3 c = curl_e_at(g, b.Ea, o, g.PP, g.F[2], true, true, true);
+        double* w = v + (size_t)q * 12;
+        w[0] = b.Ha[0][o]; w[1] = b.Ha[1][o]; w[2] = b.Ha[2][o];
+        w[3] = b.Ma[0][om]; w[4] = b.Ma[1][om]; w[5] = b.Ma[2][om];
+        w[6] = c.x; w[7] = c.y; w[8] = c.z;
+        w[9] = w[3]; w[10] = w[4]; w[11] = w[5];
+    }
+    double prev = __longlong_as_double(0x7ff0000000000000LL);
+    int growth = 0, rstar = 0, failed = 0;
+    double fres = 0.0; int fit = 0, fkind = 0;
+    for (int r = 1; r <= g.max_iters; ++r) {
+        unsigned long long lmax = 0ull;
+        for (int q = tid; q < nmag; q += nth) {
+            const int i = cells[q].x, f = cells[q].y;
+            const int64_t o = i * g.PP + f;
+            double* w = v + (size_t)q * 12;
+            LlgCell s;
+            for (int c = 0; c < 3; ++c) { s.Hn[c] = w[c]; s.Mn[c] = w[3 + c]; s.cE[c] = w[6 + c]; }
+            llg_setup(s, mats[ids[o]]);
+            double Mr[3] = {w[9], w[10], w[11]};
+            double Hr[3];
+            if (r == 1) { Hr[0] = s.Hn[0]; Hr[1] = s.Hn[1]; Hr[2] = s.Hn[2]; }
+            else {
+                for (int c = 0; c < 3; ++c)
+                    Hr[c] = (s.Hn[c] + (s.Mn[c] - Mr[c])) - g.coef_h * s.cE[c];
+            }
+            const unsigned long long rb = dbits(llg_iterate(s, g.coef_h, Hr, Mr));
+            lmax = rb > lmax ? rb : lmax;
+            w[9] = Mr[0]; w[10] = Mr[1]; w[11] = Mr[2];
+        }
+        // block max -> one atomic per block
+        for (int sh = 16; sh > 0; sh >>= 1) {
+            const unsigned long long o2 = __shfl_xor_sync(0xffffffffu, lmax, sh);
+            lmax = o2 > lmax ? o2 : lmax;
+        }
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = lmax;
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            unsigned long long x = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0ull;
+            for (int sh = 16; sh > 0; sh >>= 1) {
+                const unsigned long long o2 = __shfl_xor_sync(0xffffffffu, x, sh);
+                x = o2 > x ? o2 : x;
+            }
+            if (threadIdx.x == 0 && x) atomicMax(&st->hist2[r], x);
+        }
+        grid.sync();
+        const double res = bitsd(*((volatile unsigned long long*)&st->hist2[r]));
+        if (res <= g.tol) { rstar = r; break; }
+        growth = (res > prev) ? growth + 1 : 0;
+        if (growth >= 3) { failed = 1; fres = res; fit = r; fkind = 1; break; }
+        prev = res;
+        if (r == g.max_iters) { failed = 1; fres = prev; fit = r; fkind = 2; }
+        __syncthreads();   // red[] reuse
+    }
+    if (failed) {
+        if (tid == 0) {
+            st->fail = 1; st->fail_step = st->step; st->fail_res = fres;
+            st->fail_it = fit; st->fail_kind = fkind;
+        }
+        return;
+    }
+    for (int q = tid; q < nmag; q += nth) {
+        const int i = cells[q].x, f = cells[q].y;
+        const int64_t o = i * g.PP + f;
+        const int64_t om = (int64_t)(i - g.mx0) * g.PP + f;
+        const double* w = v + (size_t)q * 12;
+        for (int c = 0; c < 3; ++c) {
+            b.Hb[c][o] = (w[c] + (w[3 + c] - w[9 + c])) - g.coef_h * w[6 + c];
+            b.Mb[c][om] = w[9 + c];
+        }
+    }
+    if (tid == 0) st->rstar = rstar;
+}
+
+// ---------------------------------------------------------------------------
+// Walls, one launch per face in the order x0,x1,y0,y1,z0,z1 (em.py:324-359).
+// MUR1 reads the pre-update planes straight from the read buffer Ea (the
+// reference copies them before the update, em.py:306-321).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_wall(Geom g, Bufs b,
+                                              const mpb_material* __restrict__ mats,
+                                              const uint8_t* __restrict__ ids,
+                                              const StepState* st, int face) {
+    if (st->fail) return;
+    const int axis = face >> 1, side = face & 1;
+    const int u = axis == 0 ? 1 : 0;          // the two in-plane axes
+    const int w = axis == 2 ? 1 : 2;
+    const int nu = g.F[u], nw = g.F[w];
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (int64_t)nu * nw) return;
+    const int iu = (int)(t / nw), iw = (int)(t - (int64_t)iu * nw);
+    const int64_t stride[3] = {g.PP, g.F[2], 1};
+    const int wall = side == 0 ? 0 : g.n[axis];
+    const int inner = side == 0 ? 1 : g.n[axis] - 1;
+    const int64_t base = iu * stride[u] + iw * stride[w];
+    const int64_t ow = base + wall * stride[axis];
+    const int64_t oi = base + inner * stride[axis];
+    const int c0 = axis == 0 ? 1 : 0;         // tangential E components
+    const int c1 = axis == 2 ? 1 : 2;
+    if (g.faces[face] == MPB_FACE_PEC) {
+        b.Eb[c0][ow] = 0.0;
+        b.Eb[c1][ow] = 0.0;
+    } else {   // MUR1: wall = prev_inner + k (inner_new - prev_wall)
+        const double kk = mats[ids[ow]].mur_k[axis];
+        b.Eb[c0][ow] = b.Ea[c0][oi] + kk * (b.Eb[c0][oi] - b.Ea[c0][ow]);
+        b.Eb[c1][ow] = b.Ea[c1][oi] + kk * (b.Eb[c1][oi] - b.Ea[c1][ow]);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// End of step: soft source (em.py:276-282), probes (sim.py:170-171), r*
+// record (sim.py:167), reset of the LLG bookkeeping for the next step.
+// One block.
+// ---------------------------------------------------------------------------
+struct SourceDesc {
+    int64_t off;
+    double pol[3];
+};
+
+__global__ void __launch_bounds__(256) k_finish(Geom g, Bufs b, SourceDesc src,
+                                                const ProbeDesc* __restrict__ probes,
+                                                int nprobes, int parity_b, int record_iters,
+                                                StepState* st) {
+    if (st->fail) return;
+    const long long row = st->local;
+    if (threadIdx.x == 0) {
+        const double v = st->src_vals[row];
+        for (int c = 0; c < 3; ++c)
+            if (src.pol[c] != 0.0) {
+                const double pv = src.pol[c] * v;
+                b.Eb[c][src.off] = b.Eb[c][src.off] + pv;
+            }
+    }
+    __syncthreads();
+    for (int p = threadIdx.x; p < nprobes; p += blockDim.x) {
+        const ProbeDesc pd = probes[p];
+        const double* base = parity_b ? pd.ptr1 : pd.ptr0;
+        st->probe_out[row * nprobes + p] = base ? base[pd.off] : pd.constant;
+    }
+    for (int r = threadIdx.x; r <= g.max_iters + 1; r += blockDim.x) {
+        st->hist[r] = 0ull;
+        st->hist2[r] = 0ull;
+    }
+    if (threadIdx.x == 0) {
+        if (record_iters) st->iters_out[row] = st->rstar;
+        st->rstar = 0;
+        st->rc_min = 0x7fffffff;
+        st->rc_max = 0;
+        st->local = row + 1;
+        st->step = st->step + 1;
+    }
+}
+
+}  // namespace mpb

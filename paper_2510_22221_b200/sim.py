@@ -1,0 +1,227 @@
+"""Run orchestration -- the drop-in for reference ``magphon.sim``.
+
+``run(config, bias=None, resume=None) -> RunResult`` keeps the reference
+signature, return type, error behaviour and bit-for-bit results
+(reference sim.py:125-180); the time loop itself executes on the B200
+through the C ABI (``engine.DeviceRun``).  Snapshot/restart
+(sim.py:187-220) and bias sweeps (sim.py:243-260) are mirrored on top.
+
+Host work per run: material table + initial M (numpy, once), the per-step
+source values v((n+1) dt) (Python ``math``, once per step -- they must be the
+reference's exact doubles), and the final state download.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+
+from . import em, llg
+from .engine import DeviceRun
+from .grid import FieldLattice, GridSpec, initial_magnetization
+from .materials import MaterialMap
+
+_FIELD_NAMES = ("Ex", "Ey", "Ez", "Hx", "Hy", "Hz")
+_VALID_COMPS = _FIELD_NAMES + ("Mx", "My", "Mz")
+
+
+@dataclass(frozen=True)
+class SimConfig:
+    grid: GridSpec
+    materials: MaterialMap
+    source: em.SourceSpec
+    boundaries: em.BoundarySpec
+    cfl_factor: float
+    t_end: float
+    probes: tuple[tuple[str, int, int, int], ...]
+    bias_sweep: tuple[float, ...] = ()
+    bias_direction: tuple[float, float, float] = (1.0, 0.0, 0.0)
+    llg_params: llg.LlgIterationParams = field(default_factory=llg.LlgIterationParams)
+    spectrum_probe: int = 0
+
+    def __post_init__(self) -> None:
+        if not self.t_end > 0:
+            raise ValueError("t_end must be > 0")
+        for comp, i, j, k in self.probes:
+            lim = self.grid.cell_shape if comp.startswith("M") else self.grid.field_shape
+            if not all(0 <= x < n for x, n in zip((i, j, k), lim)):
+                raise ValueError(f"probe {(comp, i, j, k)} outside grid")
+
+    @property
+    def dt(self) -> float:
+        return em.cfl_timestep(self.grid, self.cfl_factor)
+
+    @property
+    def n_steps(self) -> int:
+        return int(np.ceil(self.t_end / self.dt))
+
+
+@dataclass
+class ProbeSeries:
+    component: str
+    location: tuple[int, int, int]
+    bias: float
+    dt_sample: float
+    samples: np.ndarray
+
+    def __len__(self) -> int:
+        return len(self.samples)
+
+
+@dataclass
+class RunResult:
+    probes: dict
+    lattice: FieldLattice
+    iterations: np.ndarray
+    steps: int
+    bias: float
+
+
+def _materials_with_bias(materials, bias: float, direction) -> MaterialMap:
+    """Copy with the magnetic cells' bias replaced (sim.py:82-97)."""
+    out = MaterialMap(materials.shape)
+    for name in ("sigma", "eps_r", "Ms", "alpha", "gamma_e", "Hbias"):
+        setattr(out, name, np.array(getattr(materials, name), copy=True))
+    mag = out.Ms > 0
+    unit = np.asarray(direction, float)
+    unit = unit / np.linalg.norm(unit)
+    for c in range(3):
+        out.Hbias[c][mag] = bias * unit[c]
+    return out.freeze()
+
+
+def _wrap_source(loc, shape):
+    out = []
+    for x, n in zip(loc, shape):
+        if not -n <= x < n:
+            raise IndexError(f"source index {tuple(loc)} out of bounds for "
+                             f"field shape {shape}")
+        out.append(x % n)
+    return tuple(out)
+
+
+def source_values(src: em.SourceSpec, dt: float, start: int, stop: int) -> np.ndarray:
+    """v((n+1) dt) for n in [start, stop) with the reference's Python math."""
+    return np.array([em.source_value(src, (n + 1) * dt) for n in range(start, stop)],
+                    dtype=np.float64)
+
+
+def _device_run(config, materials, keys, device: int = 0, **kw) -> DeviceRun:
+    fs = config.grid.field_shape
+    pol = config.source.polarization
+    loc = config.source.location
+    if any(p != 0.0 for p in pol):
+        loc = _wrap_source(loc, fs)
+    else:
+        loc = (0, 0, 0)
+    for comp, _ in keys:
+        if comp not in _VALID_COMPS:
+            raise KeyError(f"unknown field component {comp!r}")
+    for comp, (i, j, k) in keys:
+        lim = config.grid.cell_shape if comp.startswith("M") else fs
+        if not all(0 <= x < n for x, n in zip((i, j, k), lim)):
+            raise IndexError(f"index ({i},{j},{k}) out of range for {comp}")
+    b = config.boundaries
+    for face, axis in (("x0", 0), ("x1", 0), ("y0", 1), ("y1", 1), ("z0", 2), ("z1", 2)):
+        if getattr(b, face) == em.MUR1 and not config.grid.active_axes[axis]:
+            raise ValueError(f"MUR1 on collapsed axis face {face}")
+    return DeviceRun(config.grid, materials, b, loc, pol, keys, config.llg_params,
+                     config.dt, device=device, **kw)
+
+
+def run(config: SimConfig, bias: float | None = None, resume: dict | None = None,
+        *, device: int = 0, kernel_variant: int = 0) -> RunResult:
+    """Execute a full run on the GPU (reference sim.py:125-180).
+
+    With ``bias`` the magnets' bias is overridden along
+    ``config.bias_direction``; ``resume`` continues from a snapshot dict and
+    is bit-identical to an uninterrupted run.
+    """
+    materials = config.materials if bias is None else _materials_with_bias(
+        config.materials, bias, config.bias_direction)
+    dt = config.dt
+    n_steps = config.n_steps
+    buffers = {(p[0], (p[1], p[2], p[3])): [] for p in config.probes}
+    iters_prefix: list = []
+    start = 0
+    if resume is not None:
+        start = int(resume["step"])
+        for key, vals in resume["probes"].items():
+            buffers[key] = list(vals)
+        iters_prefix = list(resume["iterations"])
+    keys = list(buffers)
+    dev = _device_run(config, materials, keys, device=device,
+                      kernel_variant=kernel_variant)
+    try:
+        if resume is not None:
+            st = resume["fields"]
+            dev.load_state({n: st[n] for n in _FIELD_NAMES}, st["M"])
+        else:
+            zeros = np.zeros(config.grid.field_shape)
+            dev.load_state({n: zeros for n in _FIELD_NAMES},
+                           initial_magnetization(materials))
+        count = max(0, n_steps - start)
+        vals = source_values(config.source, dt, start, n_steps)
+        probe_rows, iters, fail = dev.run(start, vals)
+        if fail is not None:
+            step, res, it, kind = fail
+            if kind == 1:
+                msg = (f"fixed-point iteration diverging (residual {res:.3e} "
+                       f"after {it} iterates)")
+            else:
+                msg = (f"fixed-point iteration did not reach tol "
+                       f"{config.llg_params.tol:.1e} in "
+                       f"{config.llg_params.max_iters} iterates (residual {res:.3e})")
+            raise llg.StepFailure(msg, res, it, step=step)
+        state = dev.save_state()
+    finally:
+        dev.close()
+    lat = FieldLattice(config.grid, materials)
+    lat.load_state(state)
+    b = 0.0 if bias is None else bias
+    probes = {}
+    for p, key in enumerate(keys):
+        samples = np.concatenate([np.asarray(buffers[key], dtype=np.float64),
+                                  probe_rows[:count, p]])
+        probes[key] = ProbeSeries(component=key[0], location=key[1], bias=b,
+                                  dt_sample=dt, samples=samples)
+    if dev.n_magnetic > 0:
+        iterations = np.asarray(iters_prefix + list(iters[:count]), dtype=int)
+    else:
+        iterations = np.asarray(iters_prefix, dtype=int)
+    return RunResult(probes=probes, lattice=lat, iterations=iterations,
+                     steps=n_steps, bias=b)
+
+
+# ---------------------------------------------------------------------------
+# snapshot / restart (sim.py:187-220)
+# ---------------------------------------------------------------------------
+
+def snapshot_state(config: SimConfig, bias: float | None, until_step: int) -> dict:
+    res = run(replace(config, t_end=until_step * config.dt), bias=bias)
+    return {"fields": res.lattice.state_arrays(), "step": res.steps,
+            "probes": {k: v.samples for k, v in res.probes.items()},
+            "iterations": res.iterations}
+
+
+def save_snapshot(path, snap: dict) -> None:
+    flat = {f"field_{k}": v for k, v in snap["fields"].items()}
+    flat["step"] = np.asarray(snap["step"])
+    flat["iterations"] = np.asarray(snap["iterations"])
+    for (comp, loc), vals in snap["probes"].items():
+        flat["probe_{}_{}_{}_{}".format(comp, *loc)] = np.asarray(vals)
+    np.savez(path, **flat)
+
+
+def load_snapshot(path) -> dict:
+    data = np.load(path)
+    fields, probes = {}, {}
+    for key in data.files:
+        if key.startswith("field_"):
+            fields[key[6:]] = data[key]
+        elif key.startswith("probe_"):
+            comp, i, j, k = key[6:].rsplit("_", 3)
+            probes[(comp, (int(i), int(j), int(k)))] = data[key]
+    return {"fields": fields, "step": int(data["step"]), "probes": probes,
+            "iterations": data["iterations"]}
