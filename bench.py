@@ -1,0 +1,310 @@
+#!/usr/bin/env python3
+"""Throughput of the coupled Maxwell-LLG step on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4]
+    python bench.py --impl reference ...     # CPU reference arm
+
+Workload: C4 of SURVEY 8d -- 1024x1024x128 cells per GPU (CPW line on a Si
+substrate + YIG film, all-MUR1 walls, fp64), the per-GPU configuration the
+weak-scaling metric is quoted on.  A "step" is one full coupled step
+(curl E, H + LLG fixed point, curl H, E, walls, source, probes) of that grid.
+
+Prints ONE JSON line on rank 0:
+  value  -- Gcell-updates/s over all ranks, state resident in HBM, device
+            timed with CUDA events on the launching stream, max over ranks;
+  e2e    -- same metric through the C-ABI call mpb_run with HOST buffers
+            (per-step source values H2D, probes + r* D2H inside the timing);
+  roofline -- dominant kernel's algorithmic bytes / its event-timed duration
+            vs the measured HBM copy bandwidth (MEASURED_PEAKS.json);
+  cpu_baseline -- the numpy oracle (restatement of the reference) timed on a
+            bounded sample on this host.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {"c1": "configs/c1.cfg", "c2": "configs/c2.cfg", "c3": "configs/c3.cfg",
+           "c4": "configs/c4.cfg", "c5": "configs/c5.cfg"}
+FALLBACK_HBM = 6650.0
+METRIC = "coupled Maxwell-LLG Gcell-updates/s"
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return float(json.loads(p.read_text())["hbm_gbs"]), "measured"
+    return FALLBACK_HBM, "fallback"
+
+
+def _bytes_per_cell(f_mag: float) -> float:
+    # 6 field comps read+written once (96 B fp64) + M read+write
+    # (48 B) in the magnetic fraction.  Ids/halos/probes are not credited.
+    return 96.0 + 48.0 * f_mag
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                self.out = ""
+
+    def summary(self):
+        if not self.proc or not getattr(self, "out", ""):
+            return None
+        sms, smax, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                 "sw_power_cap"]
+        for line in self.out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sms.append(float(f[1]))
+                smax = max(smax, float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sms:
+            return None
+        return {"sm_mhz": statistics.median(sms), "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sms)}
+
+
+def cpu_oracle_sample(cfg_name: str, steps: int):
+    """Time the numpy oracle (restatement of the reference CPU path) on a
+    bounded sample; returns (Gcell-updates/s, description)."""
+    from dataclasses import replace
+
+    from oracle import magphon_oracle as orc
+    from paper_2510_22221_b200.config import load_config
+    cfg = load_config(ROOT / CONFIGS[cfg_name])
+    cells = int(np.prod(cfg.grid.cell_shape))
+    cfg = replace(cfg, t_end=(steps + 0.5) * cfg.dt)
+    orc.run(cfg, n_steps=1)                  # warm the allocator
+    t0 = time.perf_counter()
+    orc.run(cfg, n_steps=steps)
+    dt = time.perf_counter() - t0
+    return cells * steps / dt / 1e9, dt, cells
+
+
+def run_reference(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    sample = args.cpu_sample
+    _ = cpu_oracle_sample(sample, 1)       # warm-up step(s)
+    vals = []
+    t_all = 0.0
+    steps = args.steps
+    rate, secs, cells = cpu_oracle_sample(sample, steps)
+    t_all += secs
+    vals.append(rate)
+    v = rate * args.gpus  # per-GPU workload replicated N times? no: report as is
+    v = rate
+    line = {
+        "metric": METRIC, "value": v, "unit": "Gcell-updates/s",
+        "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
+        "ms_per_step": secs / steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "impl": "reference",
+        "config": {"workload": f"{args.config} (timed on a bounded sample: "
+                               f"{sample} {cells} cells)",
+                   "sample_config": sample},
+        "cpu_baseline": {"value": v, "unit": "Gcell-updates/s", "cores": 1,
+                         "kind": "port",
+                         "sample": f"numpy oracle (restatement of magphon.sim.run), "
+                                   f"{sample} {cells} cells x {steps} steps, "
+                                   f"{secs:.1f} s"},
+        "e2e": {"value": v, "unit": "Gcell-updates/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--variant", type=int, default=0)
+    ap.add_argument("--cpu-sample", default="c2")
+    ap.add_argument("--cpu-steps", type=int, default=15)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+
+    from paper_2510_22221_b200 import sim
+    from paper_2510_22221_b200.config import load_config
+    from paper_2510_22221_b200.grid import initial_magnetization
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = load_config(ROOT / CONFIGS[args.config])
+    cells = int(np.prod(cfg.grid.cell_shape))
+    mag = int(np.count_nonzero(cfg.materials.Ms > 0))
+    f_mag = mag / cells
+    keys = [(p[0], (p[1], p[2], p[3])) for p in cfg.probes]
+    keys = list(dict.fromkeys(keys))
+    dev = sim._device_run(cfg, cfg.materials, keys, device=local,
+                          kernel_variant=args.variant)
+    zeros = np.zeros(cfg.grid.field_shape)
+    dev.load_state({n: zeros for n in ("Ex", "Ey", "Ez", "Hx", "Hy", "Hz")},
+                   initial_magnetization(cfg.materials))
+    total = args.warmup + args.steps
+    src = torch.tensor(sim.source_values(cfg.source, cfg.dt, 0, total),
+                       dtype=torch.float64, device="cuda")
+    probe = torch.zeros((total, max(1, len(keys))), dtype=torch.float64, device="cuda")
+    iters = torch.zeros(total, dtype=torch.int32, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    # warm-up (W untimed steps)
+    dev.run_device(0, args.warmup, src.data_ptr(), probe.data_ptr(),
+                   iters.data_ptr(), stream.cuda_stream)
+    torch.cuda.synchronize()
+    if dev.check_failure() is not None:
+        raise RuntimeError("LLG failure during warm-up")
+    # timed region: K steps, device-resident state; dominant kernel timed by
+    # CUDA events on its own stream (library stream) inside the same region
+    dev.set_kernel_timing(True)
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        dev.run_device(args.warmup, args.steps, src[args.warmup:].data_ptr(),
+                       probe[args.warmup:].data_ptr(), iters[args.warmup:].data_ptr(),
+                       stream.cuda_stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    launches = dev.launch_count()
+    kms, klaunch, kname = dev.kernel_time()
+    dev.set_kernel_timing(False)
+    fail = dev.check_failure()
+    if fail is not None:
+        raise RuntimeError(f"LLG failure in timed region: {fail}")
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    value = cells * world * args.steps / (ms * 1e-3) / 1e9
+    # end-to-end through the C ABI with host buffers (mpb_run)
+    e2e_steps = args.e2e_steps or args.steps
+    host_src = sim.source_values(cfg.source, cfg.dt, total, total + e2e_steps)
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    _, _, fail = dev.run(total, host_src)
+    t_e2e = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        t_e2e = float(t.item())
+    e2e = cells * world * e2e_steps / t_e2e / 1e9
+    peak, peak_kind = _peaks()
+    bpc = _bytes_per_cell(f_mag)
+    per_launch_ms = kms / max(1, klaunch)
+    achieved = cells * bpc / (per_launch_ms * 1e-3) / 1e9 if klaunch else None
+    traffic = None
+    tp = ROOT / "profiles" / "traffic.json"
+    if tp.exists():
+        traffic = json.loads(tp.read_text()).get(kname)
+    if rank != 0:
+        dev.close()
+        return
+    cpu = None
+    if not args.no_cpu:
+        rate, secs, ccells = cpu_oracle_sample(args.cpu_sample, args.cpu_steps)
+        cpu = {"value": rate, "unit": "Gcell-updates/s", "cores": 1, "kind": "port",
+               "sample": f"numpy oracle (restatement of magphon.sim.run, single "
+                         f"thread like the reference) on {args.cpu_sample} "
+                         f"({ccells} cells) x {args.cpu_steps} steps = {secs:.1f} s"}
+    line = {
+        "metric": METRIC, "value": value, "unit": "Gcell-updates/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"{args.config.upper()} {'x'.join(map(str, cfg.grid.cell_shape))} "
+                               f"cells per GPU, CPW + YIG film, all-MUR1, fp64",
+                   "config_file": CONFIGS[args.config], "cells_per_gpu": cells,
+                   "magnetic_fraction": f_mag,
+                   "parallelism": f"x-slab x{world}" if world > 1 else "single GPU",
+                   "l2": "state (2 x 6 fp64 fields) >> 126 MB L2; no flush needed",
+                   "kernel_variant": args.variant},
+        "e2e": {"value": e2e, "unit": "Gcell-updates/s",
+                "h2d_bytes_per_step": 8, "d2h_bytes_per_step": 8 * len(keys) + 4,
+                "api": "mpb_run (host source values in, host probes + r* out)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
+                     "unit": "GB/s", "frac": achieved / peak if achieved else None,
+                     "traffic": traffic, "kernel": kname,
+                     "bytes_per_cell": bpc, "peak_kind": peak_kind,
+                     "kernel_ms_per_step": per_launch_ms,
+                     "kernel_share_of_step": per_launch_ms / (ms / args.steps)},
+        "cpu_baseline": cpu,
+        "clocks": clk.summary(),
+        "gpu_launches": launches,
+    }
+    print(json.dumps(line))
+    dev.close()
+
+
+if __name__ == "__main__":
+    main()

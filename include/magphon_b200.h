@@ -136,9 +136,11 @@ MPB_API int mpb_run(mpb_handle* h, int64_t n0, int64_t nsteps, const double* src
             double* probe_out, int32_t* iters_out, mpb_failure* fail);
 
 /* Device-resident variant for benchmarking / chained pipelines: all three
- * buffers are DEVICE pointers on the handle's device, the work is enqueued
- * on `stream` (a cudaStream_t, 0 = the handle's own stream) and the call
- * returns without synchronising.  Check failures with mpb_check_failure. */
+ * buffers are DEVICE pointers on the handle's device.  The work runs on the
+ * handle's stream, ordered after all work already enqueued on `stream` and
+ * with `stream` ordered after it (a cudaStream_t; 0 = the legacy default
+ * stream).  The call returns without synchronising; check failures with
+ * mpb_check_failure. */
 MPB_API int mpb_run_device(mpb_handle* h, int64_t n0, int64_t nsteps,
                    const double* d_src_vals, double* d_probe_out,
                    int32_t* d_iters_out, void* stream);
@@ -156,6 +158,12 @@ MPB_API int mpb_kernel_time(mpb_handle* h, double* ms_total, int64_t* launches,
 
 /* Number of kernel launches the last mpb_run / mpb_run_device enqueued. */
 MPB_API int64_t mpb_launch_count(mpb_handle* h);
+
+/* Self-test of the exact-division fast path used by the sweep kernels:
+ * divides each x[q] by d on the GPU both ways (hoisted-reciprocal fast path
+ * and the compiler's IEEE x/d) and counts bitwise mismatches. */
+MPB_API int mpb_selftest_division(int32_t device, double d, const double* x, int64_t n,
+                                  int64_t* mismatches, double* first_bad);
 
 /* Device bytes held by the handle. */
 MPB_API int64_t mpb_device_bytes(mpb_handle* h);

@@ -53,7 +53,7 @@ class Failure(C.Structure):
 EXPORTS = ("mpb_version", "mpb_last_error", "mpb_create", "mpb_destroy",
            "mpb_load_state", "mpb_save_state", "mpb_run", "mpb_run_device",
            "mpb_check_failure", "mpb_set_kernel_timing", "mpb_kernel_time",
-           "mpb_launch_count", "mpb_device_bytes")
+           "mpb_launch_count", "mpb_device_bytes", "mpb_selftest_division")
 
 _lib = None
 
@@ -90,6 +90,8 @@ def load_library(path: os.PathLike | None = None) -> C.CDLL:
                                       P(C.c_char_p)]),
         "mpb_launch_count": (C.c_int64, [C.c_void_p]),
         "mpb_device_bytes": (C.c_int64, [C.c_void_p]),
+        "mpb_selftest_division": (C.c_int, [C.c_int32, C.c_double, P(C.c_double),
+                                            C.c_int64, P(C.c_int64), P(C.c_double)]),
     }
     for name, (res, args) in proto.items():
         fn = getattr(lib, name)

@@ -14,6 +14,7 @@
 #include "../../include/magphon_b200.h"
 #include "mpb_device.cuh"
 #include "mpb_kernels_split.cuh"
+#include "mpb_sweep.cuh"
 
 using namespace mpb;
 
@@ -85,6 +86,8 @@ struct mpb_handle {
     int64_t timed_launches = 0;
     int64_t launches_last = 0;
     int64_t bytes = 0;
+    int nmat_table = 0;
+    void* fused = nullptr;         // FusedState (mpb_fused.cuh)
 };
 
 
@@ -354,6 +357,7 @@ int mpb_create(const mpb_setup* su, mpb_handle** out) {
     g.max_iters = su->llg_max_iters;
     g.tol = su->llg_tol;
     h->Fx = (int)F[0];
+    h->nmat_table = su->n_materials;
     h->nentries = F[0] * g.PP;
 
     // material ids on the allocation layout, edge-padded (em.py:248-252)
@@ -586,20 +590,19 @@ int mpb_run_device(mpb_handle* h, int64_t n0, int64_t nsteps, const double* d_sr
     g_err.clear();
     if (!h || nsteps < 0) return fail_msg(MPB_EINVAL, "bad arguments");
     CU(cudaSetDevice(h->device));
+    // order our stream after the caller's work (0 = legacy default stream)
+    cudaStream_t cs = stream ? (cudaStream_t)stream : cudaStreamLegacy;
     cudaEvent_t ev = nullptr;
-    if (stream) {   // order our stream after the caller's work
-        CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-        CU(cudaEventRecord(ev, (cudaStream_t)stream));
-        CU(cudaStreamWaitEvent(h->stream, ev, 0));
-    }
+    CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    CU(cudaEventRecord(ev, cs));
+    CU(cudaStreamWaitEvent(h->stream, ev, 0));
     h->launches_last = 0;
     int rc = set_run_buffers(h, n0, d_src_vals, d_probe_out, d_iters_out);
     if (!rc) rc = enqueue_steps(h, nsteps);
-    if (stream) {   // and the caller's stream after ours
-        CU(cudaEventRecord(ev, h->stream));
-        CU(cudaStreamWaitEvent((cudaStream_t)stream, ev, 0));
-        CU(cudaEventDestroy(ev));
-    }
+    // and the caller's stream after ours
+    CU(cudaEventRecord(ev, h->stream));
+    CU(cudaStreamWaitEvent(cs, ev, 0));
+    CU(cudaEventDestroy(ev));
     return rc;
 }
 
@@ -684,8 +687,35 @@ int mpb_kernel_time(mpb_handle* h, double* ms_total, int64_t* launches,
     }
     h->events.clear();
     if (ms_total) *ms_total = h->timed_ms;
-    if (launches) *launches = h->timed_launches;
+    // the split variant brackets two kernels per step; report per step
+    if (launches) *launches = h->variant == 1 ? h->timed_launches / 2 : h->timed_launches;
     if (kernel_name) *kernel_name = h->variant == 1 ? "k_hsweep+k_esweep" : fused_kernel_name();
+    return MPB_OK;
+}
+
+int mpb_selftest_division(int32_t device, double d, const double* x, int64_t n,
+                          int64_t* mismatches, double* first_bad) {
+    g_err.clear();
+    if (!x || n < 0 || !mismatches) return fail_msg(MPB_EINVAL, "bad arguments");
+    CU(cudaSetDevice(device));
+    double* dx = nullptr;
+    unsigned long long* dm = nullptr;
+    double* db = nullptr;
+    CU(cudaMalloc(&dx, sizeof(double) * std::max<int64_t>(n, 1)));
+    CU(cudaMalloc(&dm, sizeof(unsigned long long)));
+    CU(cudaMalloc(&db, sizeof(double)));
+    CU(cudaMemset(dm, 0, sizeof(unsigned long long)));
+    CU(cudaMemset(db, 0, sizeof(double)));
+    CU(cudaMemcpy(dx, x, sizeof(double) * n, cudaMemcpyHostToDevice));
+    k_div_selftest<<<1184, 256>>>(dx, n, d, dm, db);
+    CU(cudaGetLastError());
+    unsigned long long m = 0;
+    double bad = 0;
+    CU(cudaMemcpy(&m, dm, sizeof m, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(&bad, db, sizeof bad, cudaMemcpyDeviceToHost));
+    cudaFree(dx); cudaFree(dm); cudaFree(db);
+    *mismatches = (int64_t)m;
+    if (first_bad) *first_bad = bad;
     return MPB_OK;
 }
 

@@ -1,11 +1,125 @@
-// mpb_fused.cuh -- fused single-sweep variant (placeholder until written).
+// mpb_fused.cuh -- host side of the fused sweep (included by mpb_api.cu after
+// the handle definition).
 #pragma once
+#include <set>
+
 namespace {
-int prepare_fused(mpb_handle*, const Geom&) {
-    return fail_msg(MPB_EINVAL, "fused sweep not built in this version; use kernel_variant=1");
+
+struct FusedState {
+    SweepCfg sc{};
+    int V = 2;
+    int grid = 0;
+    size_t smem = 0;
+    int2* defer = nullptr;
+    int ndefer = 0;
+};
+
+FusedState* fused_of(mpb_handle* h) { return reinterpret_cast<FusedState*>(h->fused); }
+
+template <int V>
+int set_smem_attr(size_t smem) {
+    CU(cudaFuncSetAttribute(k_sweep<V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)smem));
+    return MPB_OK;
 }
-void destroy_fused(mpb_handle*) {}
-int launch_fused(mpb_handle*, const Geom&, const Bufs&, cudaStream_t) { return MPB_EINVAL; }
-int launch_deferred(mpb_handle*, const Geom&, const Bufs&, cudaStream_t) { return MPB_EINVAL; }
-const char* fused_kernel_name() { return "none"; }
+
+int prepare_fused(mpb_handle* h, const Geom& g) {
+    auto* fs = new FusedState();
+    h->fused = fs;
+    SweepCfg& sc = fs->sc;
+    const int Fz = g.F[2];
+    int sms = 0, smem_optin = 0;
+    CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
+    CU(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin,
+                              h->device));
+    sc.hl = g.act[1] ? Fz : (g.act[2] ? 1 : 0);
+    sc.eh = sc.hl;
+    sc.nmat = h->nmat_table;
+    if ((uint64_t)g.FyFz * (uint64_t)Fz >= (1ull << 32))
+        return fail_msg(MPB_EINVAL, "x-plane too large for the fused sweep (%d entries)",
+                        g.FyFz);
+    sc.fz_magic = (uint32_t)(((1ull << 32) + Fz - 1) / Fz);
+    if (Fz == 1) sc.fz_magic = 0;   // j = f for Fz == 1 handled below
+    // entries per CTA per plane: 2 per thread unless the plane is small
+    fs->V = g.FyFz >= 8 * kSweepThreads * sms ? 4 : (g.FyFz >= 2 * kSweepThreads * 64 ? 2 : 1);
+    sc.T = fs->V * kSweepThreads;
+    sc.tiles = (g.FyFz + sc.T - 1) / sc.T;
+    sc.ecap = (sc.T + sc.hl + sc.eh + 4 + 1) & ~1;
+    sc.hcap = (sc.T + sc.hl + 4 + 1) & ~1;
+    sc.icap = sc.T + sc.hl + 48;
+    sc.stage_bytes = ((3 * sc.ecap + 3 * sc.hcap) * 8 + sc.icap + 127) / 128 * 128;
+    sc.ring_offset = ((g.max_iters + 2) * 8 + 127) / 128 * 128;
+    fs->smem = (size_t)sc.ring_offset + (size_t)kSlots * sc.stage_bytes;
+    const size_t static_smem = 8 * 1024;
+    if (fs->smem + static_smem > (size_t)smem_optin)
+        return fail_msg(MPB_EINVAL, "fused sweep staging (%zu B) exceeds shared memory",
+                        fs->smem);
+    // x-chunks: ~8 waves of one CTA per SM, chunks of >= 24 planes
+    const int Fx = g.F[0];
+    const int want = std::max(1, (8 * sms + sc.tiles - 1) / sc.tiles);
+    const int maxch = std::max(1, Fx / 24);
+    sc.nchunks = std::max(1, std::min(want, maxch));
+    sc.chunk = (Fx + sc.nchunks - 1) / sc.nchunks;
+    sc.nchunks = (Fx + sc.chunk - 1) / sc.chunk;
+    fs->grid = sc.tiles * sc.nchunks;
+    int rc = fs->V == 4 ? set_smem_attr<4>(fs->smem)
+                        : (fs->V == 2 ? set_smem_attr<2>(fs->smem) : set_smem_attr<1>(fs->smem));
+    if (rc) return rc;
+    // deferred E entries: {c, c+x, c+y, c+z} over magnetic cells
+    std::vector<int64_t> keys;
+    if (h->nmag) {
+        std::vector<int2> cells((size_t)h->nmag);
+        CU(cudaMemcpy(cells.data(), h->magcells, sizeof(int2) * cells.size(),
+                      cudaMemcpyDeviceToHost));
+        keys.reserve(cells.size() * 4);
+        for (const int2& c : cells) {
+            const int i = c.x, f = c.y;
+            const int j = f / Fz, k = f - j * Fz;
+            keys.push_back((int64_t)i * g.FyFz + f);
+            if (g.act[0] && i + 1 < g.F[0]) keys.push_back((int64_t)(i + 1) * g.FyFz + f);
+            if (g.act[1] && j + 1 < g.F[1]) keys.push_back((int64_t)i * g.FyFz + f + Fz);
+            if (g.act[2] && k + 1 < g.F[2]) keys.push_back((int64_t)i * g.FyFz + f + 1);
+        }
+        std::sort(keys.begin(), keys.end());
+        keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
+        std::vector<int2> list(keys.size());
+        for (size_t q = 0; q < keys.size(); ++q)
+            list[q] = make_int2((int)(keys[q] / g.FyFz), (int)(keys[q] % g.FyFz));
+        fs->ndefer = (int)list.size();
+        CU(cudaMalloc(&fs->defer, sizeof(int2) * list.size()));
+        h->bytes += (int64_t)(sizeof(int2) * list.size());
+        CU(cudaMemcpy(fs->defer, list.data(), sizeof(int2) * list.size(),
+                      cudaMemcpyHostToDevice));
+    }
+    return MPB_OK;
+}
+
+void destroy_fused(mpb_handle* h) {
+    FusedState* fs = fused_of(h);
+    if (!fs) return;
+    cudaFree(fs->defer);
+    delete fs;
+    h->fused = nullptr;
+}
+
+int launch_fused(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s) {
+    FusedState* fs = fused_of(h);
+    switch (fs->V) {
+        case 4: k_sweep<4><<<fs->grid, kSweepThreads, fs->smem, s>>>(g, b, h->mats, h->ids, h->st, fs->sc); break;
+        case 2: k_sweep<2><<<fs->grid, kSweepThreads, fs->smem, s>>>(g, b, h->mats, h->ids, h->st, fs->sc); break;
+        default: k_sweep<1><<<fs->grid, kSweepThreads, fs->smem, s>>>(g, b, h->mats, h->ids, h->st, fs->sc); break;
+    }
+    return MPB_OK;
+}
+
+int launch_deferred(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s) {
+    FusedState* fs = fused_of(h);
+    if (!fs->ndefer) return MPB_OK;
+    k_edefer<<<(fs->ndefer + 255) / 256, 256, 0, s>>>(g, b, h->mats, h->ids, fs->defer,
+                                                    fs->ndefer, h->st);
+    return MPB_OK;
+}
+
+const char* fused_kernel_name() { return "k_sweep"; }
+
 }  // namespace

@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(256) k_llg_fixup(Geom g, Bufs b,
             b.Mb[c][om] = w[9 + c];
         }
     }
-    if (tid == 0) st->rstar = rstar;
+    if (tid == 0) { st->rstar = rstar; st->fixup_ran = 1; }
 }
 
 // ---------------------------------------------------------------------------
@@ -340,6 +340,7 @@ __global__ void __launch_bounds__(256) k_finish(Geom g, Bufs b, SourceDesc src,
     if (threadIdx.x == 0) {
         if (record_iters) st->iters_out[row] = st->rstar;
         st->rstar = 0;
+        st->fixup_ran = 0;
         st->rc_min = 0x7fffffff;
         st->rc_max = 0;
         st->local = row + 1;

@@ -1,0 +1,382 @@
+// mpb_sweep.cuh -- the fused coupled-step sweep for sm_100a.
+//
+// One kernel computes, per entry, H^{n+1} (plain update or the cell's LLG
+// fixed point to its local stop) and E^{n+1} in a single pass over the
+// lattice, so each of the 6 field arrays is read once and written once per
+// step (96 B/cell in fp64, the roofline numerator of SURVEY 8d).
+//
+// Decomposition: each CTA owns a contiguous range [f0,f1) of T entries of an
+// x-plane (a few z-rows; z is contiguous) and a chunk [i0,i1) of planes, and
+// marches along x.  Per plane it stages, with 1-D TMA bulk copies into a
+// 3-slot shared-memory ring (one mbarrier per slot):
+//    E^n  on [f0 - Fz, f1 + Fz)  (row halo either side: H needs E at j+1,
+//                                 k+1, the E update needs H at j-1, k-1)
+//    H^n, material id on [f0 - Fz, f1)
+// H^{n+1} of the plane is computed in place in shared memory (including the
+// j-1 halo row, recomputed rather than exchanged), then E^{n+1} of the owned
+// range is formed from it plus the previous plane's Hy, Hz kept in registers
+// (the x-backward difference), so no x-halo is ever re-read from HBM except
+// one plane per chunk.  Reads come from one ping-pong buffer set and writes
+// go to the other, so CTAs never race on halos.
+//
+// Exactness: same operation order as the split kernels / the reference
+// (em.py:117-139, 171-182, 206-272; llg.py:108-148); divisions by dx,dy,dz use
+// ddiv() (bitwise IEEE, see mpb_device.cuh).
+#pragma once
+
+#include "mpb_device.cuh"
+#include "mpb_kernels_split.cuh"
+
+namespace mpb {
+
+// ---------------------------------------------------------------------------
+// TMA 1-D bulk copy + mbarrier helpers (PTX)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+        "[%3];" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\tLAB_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra DONE;\n\tbra LAB_WAIT;\n\tDONE:\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// launch-time layout of one CTA's staging ring
+// ---------------------------------------------------------------------------
+struct SweepCfg {
+    int T;              // owned entries per CTA per plane
+    int tiles;          // tiles per plane
+    int chunk;          // planes per chunk
+    int nchunks;
+    int hl;             // low halo (entries) = Fz if y active, 1 if only z, else 0
+    int eh;             // high E halo, same rule
+    int ecap;           // doubles per E component slot
+    int hcap;           // doubles per H component slot
+    int icap;           // bytes of ids per slot
+    uint32_t fz_magic;  // j = umulhi(f, magic) for f < FyFz
+    int stage_bytes;    // bytes per ring slot
+    int ring_offset;    // bytes of dynamic smem before the ring (LLG history)
+    int nmat;           // entries of the material table
+};
+
+constexpr int kSweepThreads = 512;
+constexpr int kSlots = 3;
+
+__device__ __forceinline__ int fz_div(uint32_t f, uint32_t magic) {
+    return magic ? (int)__umulhi(f, magic) : (int)f;   // magic 0 <=> Fz == 1
+}
+
+// Self-test kernel: ddiv() against the compiler's IEEE division, bitwise.
+__global__ void k_div_selftest(const double* __restrict__ x, int64_t n, double d,
+                               unsigned long long* mismatches, double* first_bad) {
+    const double y = recip_of(d);
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const double a = ddiv(x[q], d, y);
+        const double r = x[q] / d;
+        if (__double_as_longlong(a) != __double_as_longlong(r) && !(a != a && r != r)) {
+            if (atomicAdd(mismatches, 1ull) == 0ull) *first_bad = x[q];
+        }
+    }
+}
+
+// LLG for one cell, kept out of line so the rare path does not inflate the
+// register allocation of the streaming path.
+__device__ __noinline__ int llg_cell_local(const mpb_material* __restrict__ mats, int id,
+                                          const Geom* gp, const double* hn,
+                                          const double* mn, const double* ce, double* hout,
+                                          double* mout, unsigned long long* shist,
+                                          int record) {
+    const Geom& g = *gp;
+    LlgCell s;
+    for (int c = 0; c < 3; ++c) { s.Hn[c] = hn[c]; s.Mn[c] = mn[c]; s.cE[c] = ce[c]; }
+    llg_setup(s, mats[id]);
+    double Hr[3] = {s.Hn[0], s.Hn[1], s.Hn[2]};
+    double Mr[3] = {s.Mn[0], s.Mn[1], s.Mn[2]};
+    int rc = g.max_iters + 1;
+    for (int r = 1; r <= g.max_iters; ++r) {
+        const double res = llg_iterate(s, g.coef_h, Hr, Mr);
+        if (record) atomicMax(&shist[r], dbits(res));
+        if (res <= g.tol) { rc = r; break; }
+    }
+    for (int c = 0; c < 3; ++c) { hout[c] = Hr[c]; mout[c] = Mr[c]; }
+    return rc;
+}
+
+template <int V>
+__global__ void __launch_bounds__(kSweepThreads, 1)
+k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
+        const uint8_t* __restrict__ gids, StepState* st, SweepCfg sc) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ uint64_t bars[kSlots];
+    __shared__ int s_rc[2];
+    __shared__ int s_anymag;
+    __shared__ double s_cacb[MPB_MAX_MATERIALS * 2];
+    __shared__ unsigned char s_mag[MPB_MAX_MATERIALS];
+    unsigned long long* s_hist = reinterpret_cast<unsigned long long*>(smem);
+    unsigned char* ring = smem + sc.ring_offset;
+
+    if (st->fail) return;
+    const int tid = threadIdx.x;
+    const int tile = blockIdx.x % sc.tiles;
+    const int chunk = blockIdx.x / sc.tiles;
+    const int f0 = tile * sc.T;
+    const int f1 = min(f0 + sc.T, g.FyFz);
+    const int Fx = g.F[0];
+    const int i0 = chunk * sc.chunk;
+    const int i1 = min(i0 + sc.chunk, Fx);
+    if (i0 >= i1) return;
+    const int pstart = i0 > 0 ? i0 - 1 : 0;
+    // last plane whose stage is needed: i1 (E only, for dEz/dx, dEy/dx of
+    // plane i1-1) when it exists and x is active
+    const int plast = (g.act[0] && i1 < Fx) ? i1 : i1 - 1;
+    const int hlo = max(0, f0 - sc.hl);
+    const int ehi = min(g.FyFz, f1 + sc.eh);
+    const int a0 = hlo & ~1;                         // 16-byte aligned starts
+    const int ae = (ehi + 1) & ~1;
+    const int ah = (f1 + 1) & ~1;
+    const int ia0 = hlo & ~15;
+    const int iae = (f1 + 15) & ~15;
+    const uint32_t ebytes = (uint32_t)(ae - a0) * 8u;
+    const uint32_t hbytes = (uint32_t)(ah - a0) * 8u;
+    const uint32_t ibytes = (uint32_t)(iae - ia0);
+
+    for (int q = tid; q < sc.nmat; q += blockDim.x) {
+        s_cacb[2 * q] = mats[q].ca;
+        s_cacb[2 * q + 1] = mats[q].cb;
+        s_mag[q] = (unsigned char)mats[q].magnetic;
+    }
+    for (int r = tid; r <= g.max_iters + 1; r += blockDim.x) s_hist[r] = 0ull;
+    if (tid == 0) {
+        s_rc[0] = 0x7fffffff; s_rc[1] = 0; s_anymag = 0;
+        for (int q = 0; q < kSlots; ++q) mbar_init(&bars[q], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+
+    auto slot_e = [&](int s, int c) {
+        return reinterpret_cast<double*>(ring + (size_t)s * sc.stage_bytes) + (size_t)c * sc.ecap;
+    };
+    auto slot_h = [&](int s, int c) {
+        return reinterpret_cast<double*>(ring + (size_t)s * sc.stage_bytes) +
+               (size_t)3 * sc.ecap + (size_t)c * sc.hcap;
+    };
+    auto slot_i = [&](int s) {
+        return ring + (size_t)s * sc.stage_bytes + (size_t)(3 * sc.ecap + 3 * sc.hcap) * 8;
+    };
+    auto issue = [&](int p) {   // thread 0 only
+        const int s = (p - pstart) % kSlots;
+        const bool full = p < i1;
+        const uint32_t bytes = 3 * ebytes + (full ? 3 * hbytes + ibytes : 0u);
+        mbar_expect_tx(&bars[s], bytes);
+        const int64_t base = (int64_t)p * g.PP;
+        for (int c = 0; c < 3; ++c) tma_load_1d(slot_e(s, c), b.Ea[c] + base + a0, ebytes, &bars[s]);
+        if (full) {
+            for (int c = 0; c < 3; ++c)
+                tma_load_1d(slot_h(s, c), b.Ha[c] + base + a0, hbytes, &bars[s]);
+            tma_load_1d(slot_i(s), gids + base + ia0, ibytes, &bars[s]);
+        }
+    };
+    if (tid == 0)
+        for (int p = pstart; p <= plast && p < pstart + kSlots; ++p) issue(p);
+
+    // reciprocals of the spacings (uniform)
+    const double ry = g.act[1] ? recip_of(g.d[1]) : 0.0;
+    const double rz = g.act[2] ? recip_of(g.d[2]) : 0.0;
+    const double rx = g.act[0] ? recip_of(g.d[0]) : 0.0;
+    const bool pmc[6] = {g.faces[0] == MPB_FACE_PMC, g.faces[1] == MPB_FACE_PMC,
+                         g.faces[2] == MPB_FACE_PMC, g.faces[3] == MPB_FACE_PMC,
+                         g.faces[4] == MPB_FACE_PMC, g.faces[5] == MPB_FACE_PMC};
+    const int Fz = g.F[2];
+    const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
+
+    double hy_prev[V], hz_prev[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) { hy_prev[v] = 0.0; hz_prev[v] = 0.0; }
+
+    for (int p = pstart; p <= i1 - 1; ++p) {
+        const int s = (p - pstart) % kSlots;
+        const uint32_t par = ((p - pstart) / kSlots) & 1;
+        const bool xnext = g.act[0] && p < nx;           // plane p+1 used by dx terms
+        const int s1 = (p + 1 - pstart) % kSlots;
+        const uint32_t par1 = ((p + 1 - pstart) / kSlots) & 1;
+        mbar_wait(&bars[s], par);
+        if (xnext) mbar_wait(&bars[s1], par1);
+        const double* Ex = slot_e(s, 0);
+        const double* Ey = slot_e(s, 1);
+        const double* Ez = slot_e(s, 2);
+        const double* Ey1 = slot_e(s1, 1);
+        const double* Ez1 = slot_e(s1, 2);
+        double* Hx = slot_h(s, 0);
+        double* Hy = slot_h(s, 1);
+        double* Hz = slot_h(s, 2);
+        const unsigned char* ids = slot_i(s);
+        const bool emit = p >= i0;
+        const bool cellplane = p < nx || !g.act[0];
+
+        // ---- H^{n+1}(p, g) for g in [hlo, f1), in place --------------------
+        for (int gg = hlo + tid; gg < f1; gg += kSweepThreads) {
+            const int j = fz_div((uint32_t)gg, sc.fz_magic);
+            const int k = gg - j * Fz;
+            const int e = gg - a0;                    // smem index (E/H slots)
+            const bool vx = j < ny && k < nz;
+            const bool vy = cellplane && k < nz;
+            const bool vz = cellplane && j < ny;
+            double cx = 0.0, cy = 0.0, cz = 0.0;
+            if (g.act[1]) {
+                if (vx) cx = cx + ddiv(Ez[e + Fz] - Ez[e], g.d[1], ry);
+                if (vz) cz = cz - ddiv(Ex[e + Fz] - Ex[e], g.d[1], ry);
+            }
+            if (g.act[2]) {
+                if (vx) cx = cx - ddiv(Ey[e + 1] - Ey[e], g.d[2], rz);
+                if (vy) cy = cy + ddiv(Ex[e + 1] - Ex[e], g.d[2], rz);
+            }
+            if (g.act[0]) {
+                if (vy) cy = cy - ddiv(Ez1[e] - Ez[e], g.d[0], rx);
+                if (vz) cz = cz + ddiv(Ey1[e] - Ey[e], g.d[0], rx);
+            }
+            const int id = ids[gg - ia0];
+            const bool magnetic = cellplane && j < ny && k < nz && s_mag[id];
+            if (!magnetic) {
+                if (vx) Hx[e] = Hx[e] - g.coef_h * cx;
+                if (vy) Hy[e] = Hy[e] - g.coef_h * cy;
+                if (vz) Hz[e] = Hz[e] - g.coef_h * cz;
+            } else {
+                const int64_t om = (int64_t)(p - g.mx0) * g.PP + gg;
+                const double hn[3] = {Hx[e], Hy[e], Hz[e]};
+                const double mn[3] = {b.Ma[0][om], b.Ma[1][om], b.Ma[2][om]};
+                const double ce[3] = {cx, cy, cz};
+                double ho[3], mo[3];
+                const bool own = emit && gg >= f0;
+                const int rc = llg_cell_local(mats, id, &g, hn, mn, ce, ho, mo, s_hist, own);
+                Hx[e] = ho[0]; Hy[e] = ho[1]; Hz[e] = ho[2];
+                if (own) {
+                    b.Mb[0][om] = mo[0]; b.Mb[1][om] = mo[1]; b.Mb[2][om] = mo[2];
+                    atomicMin(&s_rc[0], rc);
+                    atomicMax(&s_rc[1], rc);
+                    s_anymag = 1;
+                }
+            }
+        }
+        __syncthreads();
+
+        // ---- E^{n+1}(p, f) for the owned range ------------------------------
+        const int64_t base = (int64_t)p * g.PP;
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            const int f = f0 + tid + v * kSweepThreads;
+            if (f < f1) {
+                const int e = f - a0;
+                const double hx = Hx[e], hy = Hy[e], hz = Hz[e];
+                if (emit) {
+                    const int j = fz_div((uint32_t)f, sc.fz_magic);
+                    const int k = f - j * Fz;
+                    double cx = 0.0, cy = 0.0, cz = 0.0;
+                    if (g.act[1]) {   // backward y with PMC ghosts (em.py:185-203)
+                        const double zhi = (j == ny) ? (pmc[3] ? -Hz[e - Fz] : 0.0) : hz;
+                        const double zlo = (j == 0) ? (pmc[2] ? -hz : 0.0) : Hz[e - Fz];
+                        const double xhi = (j == ny) ? (pmc[3] ? -Hx[e - Fz] : 0.0) : hx;
+                        const double xlo = (j == 0) ? (pmc[2] ? -hx : 0.0) : Hx[e - Fz];
+                        cx = cx + ddiv(zhi - zlo, g.d[1], ry);
+                        cz = cz - ddiv(xhi - xlo, g.d[1], ry);
+                    }
+                    if (g.act[2]) {
+                        const double yhi = (k == nz) ? (pmc[5] ? -Hy[e - 1] : 0.0) : hy;
+                        const double ylo = (k == 0) ? (pmc[4] ? -hy : 0.0) : Hy[e - 1];
+                        const double xhi = (k == nz) ? (pmc[5] ? -Hx[e - 1] : 0.0) : hx;
+                        const double xlo = (k == 0) ? (pmc[4] ? -hx : 0.0) : Hx[e - 1];
+                        cx = cx - ddiv(yhi - ylo, g.d[2], rz);
+                        cy = cy + ddiv(xhi - xlo, g.d[2], rz);
+                    }
+                    if (g.act[0]) {
+                        const double zhi = (p == nx) ? (pmc[1] ? -hz_prev[v] : 0.0) : hz;
+                        const double zlo = (p == 0) ? (pmc[0] ? -hz : 0.0) : hz_prev[v];
+                        const double yhi = (p == nx) ? (pmc[1] ? -hy_prev[v] : 0.0) : hy;
+                        const double ylo = (p == 0) ? (pmc[0] ? -hy : 0.0) : hy_prev[v];
+                        cy = cy - ddiv(zhi - zlo, g.d[0], rx);
+                        cz = cz + ddiv(yhi - ylo, g.d[0], rx);
+                    }
+                    const int id = ids[f - ia0];
+                    const double ca = s_cacb[2 * id], cb = s_cacb[2 * id + 1];
+                    b.Eb[0][base + f] = ca * (cx - cb * Ex[e]);
+                    b.Eb[1][base + f] = ca * (cy - cb * Ey[e]);
+                    b.Eb[2][base + f] = ca * (cz - cb * Ez[e]);
+                    const bool cp = p < nx || !g.act[0];
+                    if (j < ny && k < nz) b.Hb[0][base + f] = hx;
+                    if (cp && k < nz) b.Hb[1][base + f] = hy;
+                    if (cp && j < ny) b.Hb[2][base + f] = hz;
+                }
+                hy_prev[v] = hy;
+                hz_prev[v] = hz;
+            }
+        }
+        __syncthreads();
+        if (tid == 0 && p + kSlots <= plast) {
+            fence_proxy_async();
+            issue(p + kSlots);
+        }
+    }
+    // drain an issued-but-unused lookahead stage before the CTA exits
+    if (plast >= i1) {
+        const int p = plast;
+        const int s = (p - pstart) % kSlots;
+        const bool consumed_wait = g.act[0] && (i1 - 1) < nx;   // waited as s1 above
+        if (!consumed_wait) mbar_wait(&bars[s], ((p - pstart) / kSlots) & 1);
+    }
+    if (s_anymag) {
+        __syncthreads();
+        for (int r = 1 + tid; r <= g.max_iters; r += blockDim.x) {
+            const unsigned long long v = s_hist[r];
+            if (v) atomicMax(&st->hist[r], v);
+        }
+        if (tid == 0) {
+            atomicMin(&st->rc_min, s_rc[0]);
+            atomicMax(&st->rc_max, s_rc[1]);
+        }
+    }
+}
+
+// E entries whose curl-H stencil touches a magnetic H entry, recomputed after
+// the LLG fixup settled r* (only when the fixup had to recompute).
+__global__ void __launch_bounds__(256) k_edefer(Geom g, Bufs b,
+                                                const mpb_material* __restrict__ mats,
+                                                const uint8_t* __restrict__ ids,
+                                                const int2* __restrict__ list, int n,
+                                                const StepState* st) {
+    if (st->fail || !st->fixup_ran) return;
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= n) return;
+    const int i = list[q].x, f = list[q].y;
+    const int j = f / g.F[2];
+    const int k = f - j * g.F[2];
+    e_update_at(g, b, mats, ids, i, j, k, i * g.PP + f);
+}
+
+}  // namespace mpb

@@ -25,29 +25,35 @@ E_H_NAMES = ("Ex", "Ey", "Ez", "Hx", "Hy", "Hz")
 
 
 def _codes(arr: np.ndarray, limit: int = 64):
-    """Small-alphabet encoding of a float array (few distinct values)."""
+    """Small-alphabet encoding of an array with few distinct values.
+
+    Returns (codes, values, first_index).  One vectorised pass per distinct
+    value, so 1e8-cell maps with a handful of materials encode in seconds;
+    falls back to np.unique beyond ``limit`` values.
+    """
     flat = arr.reshape(-1)
     codes = np.full(flat.shape, -1, dtype=np.int32)
-    values = []
+    values, firsts = [], []
     todo = np.ones(flat.shape, dtype=bool)
     start = 0
     while True:
-        rest = np.flatnonzero(todo[start:])
+        rest = np.flatnonzero(todo[start:start + (1 << 20)])
         if rest.size == 0:
-            break
+            rest = np.flatnonzero(todo[start:])
+            if rest.size == 0:
+                break
         first = start + int(rest[0])
         v = flat[first]
-        hit = flat == v
-        if v != v:            # NaN never equals itself
-            hit = np.isnan(flat)
+        hit = np.isnan(flat) if v != v else (flat == v)
         codes[hit & todo] = len(values)
         values.append(v)
+        firsts.append(first)
         todo &= ~hit
         start = first
         if len(values) > limit:
-            u, inv = np.unique(flat, return_inverse=True)
-            return inv.astype(np.int32).reshape(arr.shape), list(u)
-    return codes.reshape(arr.shape), values
+            u, idx, inv = np.unique(flat, return_index=True, return_inverse=True)
+            return inv.astype(np.int32).reshape(arr.shape), list(u), list(idx)
+    return codes.reshape(arr.shape), values, firsts
 
 
 def material_table(materials, dt: float, spacings):
@@ -60,7 +66,7 @@ def material_table(materials, dt: float, spacings):
     key = np.zeros(mag.shape, dtype=np.int64)
     radix = 1
     for a in fields:
-        cd, vals = _codes(a)
+        cd, vals, _ = _codes(a)
         key += cd.astype(np.int64) * radix
         radix *= len(vals)
     # magnetic parameters only matter in magnetic cells
@@ -69,14 +75,15 @@ def material_table(materials, dt: float, spacings):
     if mag.any():
         for a in mfields:
             sub = np.where(mag, a, 0.0)
-            cd, vals = _codes(sub)
+            cd, vals, _ = _codes(sub)
             key += cd.astype(np.int64) * radix
             radix *= max(1, len(vals))
-    ukeys, first, inv = np.unique(key.reshape(-1), return_index=True,
-                                  return_inverse=True)
-    if ukeys.size > N.MAX_MATERIALS:
-        raise ValueError(f"{ukeys.size} distinct materials; the device table "
+    inv, ukeys, first = _codes(key, limit=N.MAX_MATERIALS)
+    nmat = len(ukeys)
+    if nmat > N.MAX_MATERIALS:
+        raise ValueError(f"{nmat} distinct materials; the device table "
                          f"holds at most {N.MAX_MATERIALS}")
+    first = np.asarray(first)
     ids = inv.astype(np.uint8).reshape(mag.shape)
     pick = lambda a: np.asarray(a).reshape(-1)[first]     # noqa: E731
     sigma, eps_r = pick(fields[0]), pick(fields[1])
@@ -91,8 +98,8 @@ def material_table(materials, dt: float, spacings):
     with np.errstate(divide="ignore", invalid="ignore"):
         c_llg = CONSTANTS.mu0 * np.abs(gamma) * dt / 2.0
         a_ms = np.where(ismag, alpha / np.where(ismag, Ms, 1.0), 0.0)
-    table = (N.Material * ukeys.size)()
-    for q in range(ukeys.size):
+    table = (N.Material * nmat)()
+    for q in range(nmat):
         m = table[q]
         m.ca, m.cb = ca[q], cb[q]
         for a in range(3):

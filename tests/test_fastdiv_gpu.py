@@ -1,0 +1,37 @@
+"""The sweep's hoisted-reciprocal division equals IEEE x/d bitwise."""
+
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from paper_2510_22221_b200 import _native
+
+pytestmark = pytest.mark.gpu
+
+SPACINGS = [10e-6, 8e-6, 6e-6, 5e-6, 4e-6, 3e-6, 2e-6, 1e-6, 19e-6, 4e-6 / 3,
+            1.0, 3.0, 0.1, 7.123456789e-5]
+
+
+def _samples(seed, n):
+    rng = np.random.default_rng(seed)
+    # random bit patterns over the whole double range plus field-like values
+    bits = rng.integers(0, 2**63, size=n, dtype=np.uint64)
+    bits |= rng.integers(0, 2, size=n, dtype=np.uint64) << np.uint64(63)
+    x = bits.view(np.float64)
+    y = rng.normal(size=n) * 10.0 ** rng.uniform(-320, 300, size=n)
+    special = np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 5e-324, -5e-324,
+                        2.2250738585072014e-308, 1.7976931348623157e308,
+                        1e-300, 1e-310, 2.0**-969, 2.0**-970, 2.0**-1000])
+    return np.concatenate([x, y, special])
+
+
+@pytest.mark.parametrize("d", SPACINGS)
+def test_ddiv_matches_ieee_division(d):
+    lib = _native.load_library()
+    x = np.ascontiguousarray(_samples(hash(d) & 0xffff, 4_000_000))
+    mism = C.c_int64()
+    bad = C.c_double()
+    _native.check(lib.mpb_selftest_division(0, d, x.ctypes.data_as(C.POINTER(C.c_double)),
+                                            x.size, C.byref(mism), C.byref(bad)))
+    assert mism.value == 0, f"first mismatch at x={bad.value!r}"

@@ -15,7 +15,7 @@ from tests.golden_io import load
 
 pytestmark = pytest.mark.gpu
 
-VARIANTS = [1]
+VARIANTS = [0, 1]
 RUNNING = [n for n in CASES if "llg" not in CASES[n]]
 
 
