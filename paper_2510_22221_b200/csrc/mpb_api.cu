@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -317,7 +318,8 @@ int mpb_create(const mpb_setup* su, mpb_handle** out) {
     *out = nullptr;
     for (int a = 0; a < 3; ++a) {
         if (su->n[a] < 1) return fail_msg(MPB_EINVAL, "cell counts must be >= 1");
-        if (!(su->d[a] > 0)) return fail_msg(MPB_EINVAL, "cell sizes must be > 0");
+        if (!(su->d[a] > 0) || !std::isfinite(su->d[a]))
+            return fail_msg(MPB_EINVAL, "cell sizes must be finite and > 0");
     }
     if (su->n_materials < 1 || su->n_materials > MPB_MAX_MATERIALS)
         return fail_msg(MPB_EINVAL, "need 1..%d materials, got %d", MPB_MAX_MATERIALS,

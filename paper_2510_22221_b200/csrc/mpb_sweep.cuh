@@ -130,6 +130,49 @@ __device__ __noinline__ int llg_cell_local(const mpb_material* __restrict__ mats
     return rc;
 }
 
+// H^{n+1} at one entry of the staged plane (in place in shared memory).
+// Straight-line: all six differences and divisions are issued back to back
+// and the division guard is checked once for the batch.
+struct HCtx {
+    const double* Ex; const double* Ey; const double* Ez;
+    const double* Ey1; const double* Ez1;
+    double* Hx; double* Hy; double* Hz;
+};
+
+__device__ __forceinline__ void h_entry(const Geom& g, const HCtx& c, int e, int j, int k,
+                                        bool cellplane, int Fz, double ry, double rz,
+                                        double rx, double& cx, double& cy, double& cz,
+                                        bool& vx, bool& vy, bool& vz) {
+    vx = j < g.n[1] && k < g.n[2];
+    vy = cellplane && k < g.n[2];
+    vz = cellplane && j < g.n[1];
+    const double ex = c.Ex[e], ey = c.Ey[e], ez = c.Ez[e];
+    const double a0 = c.Ez[e + Fz] - ez;   // dEz/dy
+    const double a1 = c.Ex[e + Fz] - ex;   // dEx/dy
+    const double a2 = c.Ey[e + 1] - ey;    // dEy/dz
+    const double a3 = c.Ex[e + 1] - ex;    // dEx/dz
+    const double a4 = c.Ez1[e] - ez;       // dEz/dx
+    const double a5 = c.Ey1[e] - ey;       // dEy/dx
+    unsigned oky = 1, okz = 1, okx = 1;
+    double q0 = ddiv_nb(a0, g.d[1], ry, oky);
+    double q1 = ddiv_nb(a1, g.d[1], ry, oky);
+    double q2 = ddiv_nb(a2, g.d[2], rz, okz);
+    double q3 = ddiv_nb(a3, g.d[2], rz, okz);
+    double q4 = ddiv_nb(a4, g.d[0], rx, okx);
+    double q5 = ddiv_nb(a5, g.d[0], rx, okx);
+    const bool bad = (g.act[1] && !oky) || (g.act[2] && !okz) || (g.act[0] && !okx);
+    if (__builtin_expect(bad, 0)) {
+        q0 = slow_div(a0, g.d[1]); q1 = slow_div(a1, g.d[1]);
+        q2 = slow_div(a2, g.d[2]); q3 = slow_div(a3, g.d[2]);
+        q4 = slow_div(a4, g.d[0]); q5 = slow_div(a5, g.d[0]);
+    }
+    // em.py:130-138 accumulation order, collapsed axes omitted
+    cx = 0.0; cy = 0.0; cz = 0.0;
+    if (g.act[1]) { cx = cx + q0; cz = cz - q1; }
+    if (g.act[2]) { cx = cx - q2; cy = cy + q3; }
+    if (g.act[0]) { cy = cy - q4; cz = cz + q5; }
+}
+
 template <int V>
 __global__ void __launch_bounds__(kSweepThreads, 1)
 k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
@@ -181,63 +224,63 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
     }
     __syncthreads();
 
-    auto slot_e = [&](int s, int c) {
-        return reinterpret_cast<double*>(ring + (size_t)s * sc.stage_bytes) + (size_t)c * sc.ecap;
+    // slot layout: E[3][ecap] | H[3][hcap] | ids[icap]
+    auto slot = [&](int p) { return (p - pstart) % kSlots; };
+    auto sE = [&](int s, int c) {
+        return reinterpret_cast<double*>(ring + (size_t)s * sc.stage_bytes) + c * sc.ecap;
     };
-    auto slot_h = [&](int s, int c) {
+    auto sH = [&](int s, int c) {
         return reinterpret_cast<double*>(ring + (size_t)s * sc.stage_bytes) +
-               (size_t)3 * sc.ecap + (size_t)c * sc.hcap;
+               3 * sc.ecap + c * sc.hcap;
     };
-    auto slot_i = [&](int s) {
-        return ring + (size_t)s * sc.stage_bytes + (size_t)(3 * sc.ecap + 3 * sc.hcap) * 8;
+    auto sI = [&](int s) {
+        return ring + (size_t)s * sc.stage_bytes + (3 * sc.ecap + 3 * sc.hcap) * 8;
     };
     auto issue = [&](int p) {   // thread 0 only
-        const int s = (p - pstart) % kSlots;
+        const int s = slot(p);
         const bool full = p < i1;
         const uint32_t bytes = 3 * ebytes + (full ? 3 * hbytes + ibytes : 0u);
         mbar_expect_tx(&bars[s], bytes);
         const int64_t base = (int64_t)p * g.PP;
-        for (int c = 0; c < 3; ++c) tma_load_1d(slot_e(s, c), b.Ea[c] + base + a0, ebytes, &bars[s]);
+        for (int c = 0; c < 3; ++c) tma_load_1d(sE(s, c), b.Ea[c] + base + a0, ebytes, &bars[s]);
         if (full) {
             for (int c = 0; c < 3; ++c)
-                tma_load_1d(slot_h(s, c), b.Ha[c] + base + a0, hbytes, &bars[s]);
-            tma_load_1d(slot_i(s), gids + base + ia0, ibytes, &bars[s]);
+                tma_load_1d(sH(s, c), b.Ha[c] + base + a0, hbytes, &bars[s]);
+            tma_load_1d(sI(s), gids + base + ia0, ibytes, &bars[s]);
         }
     };
     if (tid == 0)
         for (int p = pstart; p <= plast && p < pstart + kSlots; ++p) issue(p);
 
-    // reciprocals of the spacings (uniform)
-    const double ry = g.act[1] ? recip_of(g.d[1]) : 0.0;
-    const double rz = g.act[2] ? recip_of(g.d[2]) : 0.0;
-    const double rx = g.act[0] ? recip_of(g.d[0]) : 0.0;
-    const bool pmc[6] = {g.faces[0] == MPB_FACE_PMC, g.faces[1] == MPB_FACE_PMC,
-                         g.faces[2] == MPB_FACE_PMC, g.faces[3] == MPB_FACE_PMC,
-                         g.faces[4] == MPB_FACE_PMC, g.faces[5] == MPB_FACE_PMC};
+    const double ry = g.act[1] ? recip_of(g.d[1]) : 1.0;
+    const double rz = g.act[2] ? recip_of(g.d[2]) : 1.0;
+    const double rx = g.act[0] ? recip_of(g.d[0]) : 1.0;
     const int Fz = g.F[2];
     const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
+    const bool pmc_x0 = g.faces[0] == MPB_FACE_PMC, pmc_x1 = g.faces[1] == MPB_FACE_PMC;
+    const bool pmc_y0 = g.faces[2] == MPB_FACE_PMC, pmc_y1 = g.faces[3] == MPB_FACE_PMC;
+    const bool pmc_z0 = g.faces[4] == MPB_FACE_PMC, pmc_z1 = g.faces[5] == MPB_FACE_PMC;
 
     double hy_prev[V], hz_prev[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) { hy_prev[v] = 0.0; hz_prev[v] = 0.0; }
 
     for (int p = pstart; p <= i1 - 1; ++p) {
-        const int s = (p - pstart) % kSlots;
-        const uint32_t par = ((p - pstart) / kSlots) & 1;
+        const int s = slot(p);
         const bool xnext = g.act[0] && p < nx;           // plane p+1 used by dx terms
-        const int s1 = (p + 1 - pstart) % kSlots;
-        const uint32_t par1 = ((p + 1 - pstart) / kSlots) & 1;
-        mbar_wait(&bars[s], par);
-        if (xnext) mbar_wait(&bars[s1], par1);
-        const double* Ex = slot_e(s, 0);
-        const double* Ey = slot_e(s, 1);
-        const double* Ez = slot_e(s, 2);
-        const double* Ey1 = slot_e(s1, 1);
-        const double* Ez1 = slot_e(s1, 2);
-        double* Hx = slot_h(s, 0);
-        double* Hy = slot_h(s, 1);
-        double* Hz = slot_h(s, 2);
-        const unsigned char* ids = slot_i(s);
+        const int s1 = slot(p + 1);
+        if (tid == 0) {
+            mbar_wait(&bars[s], ((p - pstart) / kSlots) & 1);
+            if (xnext) mbar_wait(&bars[s1], ((p + 1 - pstart) / kSlots) & 1);
+        }
+        __syncthreads();   // staged data visible; E phase of p-1 done everywhere
+        if (tid == 0 && p > pstart && p + 2 <= plast) {
+            fence_proxy_async();
+            issue(p + 2);  // into the slot plane p-1 just released
+        }
+        HCtx hc{sE(s, 0), sE(s, 1), sE(s, 2), sE(s1, 1), sE(s1, 2),
+                sH(s, 0), sH(s, 1), sH(s, 2)};
+        const unsigned char* ids = sI(s);
         const bool emit = p >= i0;
         const bool cellplane = p < nx || !g.act[0];
 
@@ -245,38 +288,25 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
         for (int gg = hlo + tid; gg < f1; gg += kSweepThreads) {
             const int j = fz_div((uint32_t)gg, sc.fz_magic);
             const int k = gg - j * Fz;
-            const int e = gg - a0;                    // smem index (E/H slots)
-            const bool vx = j < ny && k < nz;
-            const bool vy = cellplane && k < nz;
-            const bool vz = cellplane && j < ny;
-            double cx = 0.0, cy = 0.0, cz = 0.0;
-            if (g.act[1]) {
-                if (vx) cx = cx + ddiv(Ez[e + Fz] - Ez[e], g.d[1], ry);
-                if (vz) cz = cz - ddiv(Ex[e + Fz] - Ex[e], g.d[1], ry);
-            }
-            if (g.act[2]) {
-                if (vx) cx = cx - ddiv(Ey[e + 1] - Ey[e], g.d[2], rz);
-                if (vy) cy = cy + ddiv(Ex[e + 1] - Ex[e], g.d[2], rz);
-            }
-            if (g.act[0]) {
-                if (vy) cy = cy - ddiv(Ez1[e] - Ez[e], g.d[0], rx);
-                if (vz) cz = cz + ddiv(Ey1[e] - Ey[e], g.d[0], rx);
-            }
+            const int e = gg - a0;
+            double cx, cy, cz;
+            bool vx, vy, vz;
+            h_entry(g, hc, e, j, k, cellplane, Fz, ry, rz, rx, cx, cy, cz, vx, vy, vz);
             const int id = ids[gg - ia0];
             const bool magnetic = cellplane && j < ny && k < nz && s_mag[id];
-            if (!magnetic) {
-                if (vx) Hx[e] = Hx[e] - g.coef_h * cx;
-                if (vy) Hy[e] = Hy[e] - g.coef_h * cy;
-                if (vz) Hz[e] = Hz[e] - g.coef_h * cz;
+            if (__builtin_expect(!magnetic, 1)) {
+                if (vx) hc.Hx[e] = hc.Hx[e] - g.coef_h * cx;
+                if (vy) hc.Hy[e] = hc.Hy[e] - g.coef_h * cy;
+                if (vz) hc.Hz[e] = hc.Hz[e] - g.coef_h * cz;
             } else {
                 const int64_t om = (int64_t)(p - g.mx0) * g.PP + gg;
-                const double hn[3] = {Hx[e], Hy[e], Hz[e]};
+                const double hn[3] = {hc.Hx[e], hc.Hy[e], hc.Hz[e]};
                 const double mn[3] = {b.Ma[0][om], b.Ma[1][om], b.Ma[2][om]};
                 const double ce[3] = {cx, cy, cz};
                 double ho[3], mo[3];
                 const bool own = emit && gg >= f0;
                 const int rc = llg_cell_local(mats, id, &g, hn, mn, ce, ho, mo, s_hist, own);
-                Hx[e] = ho[0]; Hy[e] = ho[1]; Hz[e] = ho[2];
+                hc.Hx[e] = ho[0]; hc.Hy[e] = ho[1]; hc.Hz[e] = ho[2];
                 if (own) {
                     b.Mb[0][om] = mo[0]; b.Mb[1][om] = mo[1]; b.Mb[2][om] = mo[2];
                     atomicMin(&s_rc[0], rc);
@@ -288,6 +318,9 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
         __syncthreads();
 
         // ---- E^{n+1}(p, f) for the owned range ------------------------------
+        const double* Hx = hc.Hx;
+        const double* Hy = hc.Hy;
+        const double* Hz = hc.Hz;
         const int64_t base = (int64_t)p * g.PP;
 #pragma unroll
         for (int v = 0; v < V; ++v) {
@@ -298,33 +331,48 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
                 if (emit) {
                     const int j = fz_div((uint32_t)f, sc.fz_magic);
                     const int k = f - j * Fz;
-                    double cx = 0.0, cy = 0.0, cz = 0.0;
-                    if (g.act[1]) {   // backward y with PMC ghosts (em.py:185-203)
-                        const double zhi = (j == ny) ? (pmc[3] ? -Hz[e - Fz] : 0.0) : hz;
-                        const double zlo = (j == 0) ? (pmc[2] ? -hz : 0.0) : Hz[e - Fz];
-                        const double xhi = (j == ny) ? (pmc[3] ? -Hx[e - Fz] : 0.0) : hx;
-                        const double xlo = (j == 0) ? (pmc[2] ? -hx : 0.0) : Hx[e - Fz];
-                        cx = cx + ddiv(zhi - zlo, g.d[1], ry);
-                        cz = cz - ddiv(xhi - xlo, g.d[1], ry);
+                    const int ejm = j > 0 ? e - Fz : e;   // clamp: never read off-range
+                    const int ekm = k > 0 ? e - 1 : e;
+                    const double hz_jm = Hz[ejm], hx_jm = Hx[ejm];
+                    const double hy_km = Hy[ekm], hx_km = Hx[ekm];
+                    // backward differences with PMC ghosts (em.py:185-203)
+                    const double zhi = (j == ny) ? (pmc_y1 ? -hz_jm : 0.0) : hz;
+                    const double zlo = (j == 0) ? (pmc_y0 ? -hz : 0.0) : hz_jm;
+                    const double xhi = (j == ny) ? (pmc_y1 ? -hx_jm : 0.0) : hx;
+                    const double xlo = (j == 0) ? (pmc_y0 ? -hx : 0.0) : hx_jm;
+                    const double yhi_k = (k == nz) ? (pmc_z1 ? -hy_km : 0.0) : hy;
+                    const double ylo_k = (k == 0) ? (pmc_z0 ? -hy : 0.0) : hy_km;
+                    const double xhi_k = (k == nz) ? (pmc_z1 ? -hx_km : 0.0) : hx;
+                    const double xlo_k = (k == 0) ? (pmc_z0 ? -hx : 0.0) : hx_km;
+                    const double zhi_i = (p == nx) ? (pmc_x1 ? -hz_prev[v] : 0.0) : hz;
+                    const double zlo_i = (p == 0) ? (pmc_x0 ? -hz : 0.0) : hz_prev[v];
+                    const double yhi_i = (p == nx) ? (pmc_x1 ? -hy_prev[v] : 0.0) : hy;
+                    const double ylo_i = (p == 0) ? (pmc_x0 ? -hy : 0.0) : hy_prev[v];
+                    const double b0 = zhi - zlo, b1 = xhi - xlo, b2 = yhi_k - ylo_k;
+                    const double b3 = xhi_k - xlo_k, b4 = zhi_i - zlo_i, b5 = yhi_i - ylo_i;
+                    unsigned oky = 1, okz = 1, okx = 1;
+                    double q0 = ddiv_nb(b0, g.d[1], ry, oky);
+                    double q1 = ddiv_nb(b1, g.d[1], ry, oky);
+                    double q2 = ddiv_nb(b2, g.d[2], rz, okz);
+                    double q3 = ddiv_nb(b3, g.d[2], rz, okz);
+                    double q4 = ddiv_nb(b4, g.d[0], rx, okx);
+                    double q5 = ddiv_nb(b5, g.d[0], rx, okx);
+                    const bool bad = (g.act[1] && !oky) || (g.act[2] && !okz) ||
+                                     (g.act[0] && !okx);
+                    if (__builtin_expect(bad, 0)) {
+                        q0 = slow_div(b0, g.d[1]); q1 = slow_div(b1, g.d[1]);
+                        q2 = slow_div(b2, g.d[2]); q3 = slow_div(b3, g.d[2]);
+                        q4 = slow_div(b4, g.d[0]); q5 = slow_div(b5, g.d[0]);
                     }
-                    if (g.act[2]) {
-                        const double yhi = (k == nz) ? (pmc[5] ? -Hy[e - 1] : 0.0) : hy;
-                        const double ylo = (k == 0) ? (pmc[4] ? -hy : 0.0) : Hy[e - 1];
-                        const double xhi = (k == nz) ? (pmc[5] ? -Hx[e - 1] : 0.0) : hx;
-                        const double xlo = (k == 0) ? (pmc[4] ? -hx : 0.0) : Hx[e - 1];
-                        cx = cx - ddiv(yhi - ylo, g.d[2], rz);
-                        cy = cy + ddiv(xhi - xlo, g.d[2], rz);
-                    }
-                    if (g.act[0]) {
-                        const double zhi = (p == nx) ? (pmc[1] ? -hz_prev[v] : 0.0) : hz;
-                        const double zlo = (p == 0) ? (pmc[0] ? -hz : 0.0) : hz_prev[v];
-                        const double yhi = (p == nx) ? (pmc[1] ? -hy_prev[v] : 0.0) : hy;
-                        const double ylo = (p == 0) ? (pmc[0] ? -hy : 0.0) : hy_prev[v];
-                        cy = cy - ddiv(zhi - zlo, g.d[0], rx);
-                        cz = cz + ddiv(yhi - ylo, g.d[0], rx);
-                    }
+                    double cx = 0.0, cy = 0.0, cz = 0.0;   // em.py:217-231 order
+                    if (g.act[1]) { cx = cx + q0; cz = cz - q1; }
+                    if (g.act[2]) { cx = cx - q2; cy = cy + q3; }
+                    if (g.act[0]) { cy = cy - q4; cz = cz + q5; }
                     const int id = ids[f - ia0];
                     const double ca = s_cacb[2 * id], cb = s_cacb[2 * id + 1];
+                    const double* Ex = hc.Ex;
+                    const double* Ey = hc.Ey;
+                    const double* Ez = hc.Ez;
                     b.Eb[0][base + f] = ca * (cx - cb * Ex[e]);
                     b.Eb[1][base + f] = ca * (cy - cb * Ey[e]);
                     b.Eb[2][base + f] = ca * (cz - cb * Ez[e]);
@@ -337,21 +385,9 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
                 hz_prev[v] = hz;
             }
         }
-        __syncthreads();
-        if (tid == 0 && p + kSlots <= plast) {
-            fence_proxy_async();
-            issue(p + kSlots);
-        }
     }
-    // drain an issued-but-unused lookahead stage before the CTA exits
-    if (plast >= i1) {
-        const int p = plast;
-        const int s = (p - pstart) % kSlots;
-        const bool consumed_wait = g.act[0] && (i1 - 1) < nx;   // waited as s1 above
-        if (!consumed_wait) mbar_wait(&bars[s], ((p - pstart) / kSlots) & 1);
-    }
+    __syncthreads();
     if (s_anymag) {
-        __syncthreads();
         for (int r = 1 + tid; r <= g.max_iters; r += blockDim.x) {
             const unsigned long long v = s_hist[r];
             if (v) atomicMax(&st->hist[r], v);
