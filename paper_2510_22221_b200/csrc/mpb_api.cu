@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -98,6 +99,8 @@ int prepare_fused(mpb_handle* h, const Geom& g);
 void destroy_fused(mpb_handle* h);
 int launch_fused(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s);
 int launch_deferred(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s);
+int launch_zfix(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s);
+int zfix_launches(mpb_handle* h);
 const char* fused_kernel_name();
 }  // namespace
 
@@ -198,7 +201,9 @@ int enqueue_step(mpb_handle* h, int pa, bool timed) {
     }
     if (timed && h->variant != 1) CU(cudaEventRecord(e1, s));
     if (timed) h->events.emplace_back(e0, e1);
-    for (int face = 0; face < 6; ++face) {
+    // fused variant: z walls are applied inside the sweep (+ k_zfix below)
+    const int nface = h->variant == 1 ? 6 : 4;
+    for (int face = 0; face < nface; ++face) {
         if (!h->faces_active[face]) continue;
         const int axis = face >> 1;
         const int u = axis == 0 ? 1 : 0, w = axis == 2 ? 1 : 2;
@@ -206,6 +211,11 @@ int enqueue_step(mpb_handle* h, int pa, bool timed) {
         k_wall<<<(unsigned)((cnt + 255) / 256), 256, 0, s>>>(g, b, h->mats, h->ids, h->st,
                                                             face);
         ++launches;
+    }
+    if (h->variant != 1) {
+        int rc = launch_zfix(h, g, b, s);
+        if (rc) return rc;
+        launches += zfix_launches(h);
     }
     k_finish<<<1, 256, 0, s>>>(g, b, h->src, h->probes, h->nprobes, 1 - pa,
                                h->nmag > 0 ? 1 : 0, h->st);
@@ -235,7 +245,8 @@ int build_graph(mpb_handle* h, int start_parity) {
 int64_t launches_per_step(const mpb_handle* h) {
     int64_t n = (h->variant == 1 ? 2 : 1) + 1;
     if (h->nmag > 0) n += (h->variant == 1 ? 1 : 2);
-    for (int f = 0; f < 6; ++f) n += h->faces_active[f];
+    for (int f = 0; f < (h->variant == 1 ? 6 : 4); ++f) n += h->faces_active[f];
+    if (h->variant != 1) n += zfix_launches(const_cast<mpb_handle*>(h));
     return n;
 }
 
@@ -359,9 +370,26 @@ int mpb_create(const mpb_setup* su, mpb_handle** out) {
     g.max_iters = su->llg_max_iters;
     g.tol = su->llg_tol;
     h->Fx = (int)F[0];
-    h->nmat_table = su->n_materials;
+    h->nmat_table = MPB_MAX_MATERIALS;
     h->nentries = F[0] * g.PP;
 
+    // material table renumbered so that magnetic materials carry bit 7 of
+    // the id (the sweep tests magnetism without a table lookup)
+    std::vector<int> remap((size_t)su->n_materials);
+    std::vector<mpb_material> table(MPB_MAX_MATERIALS);
+    memset(table.data(), 0, sizeof(mpb_material) * table.size());
+    {
+        int nm = 0, mm = 0;
+        for (int q = 0; q < su->n_materials; ++q) {
+            const int id = su->materials[q].magnetic ? 128 + mm++ : nm++;
+            if (nm > 128 || mm > 128) {
+                delete h;
+                return fail_msg(MPB_EINVAL, "at most 128 magnetic and 128 non-magnetic materials");
+            }
+            remap[(size_t)q] = id;
+            table[(size_t)id] = su->materials[q];
+        }
+    }
     // material ids on the allocation layout, edge-padded (em.py:248-252)
     const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
     std::vector<uint8_t> ids((size_t)h->nentries, 0);
@@ -372,14 +400,15 @@ int mpb_create(const mpb_setup* su, mpb_handle** out) {
             for (int k = 0; k < F[2]; ++k) {
                 const int ci = std::min(i, nx - 1), cj = std::min(j, ny - 1),
                           ck = std::min(k, nz - 1);
-                const uint8_t id = su->cell_material[((size_t)ci * ny + cj) * nz + ck];
-                if (id >= su->n_materials) {
+                const uint8_t id0 = su->cell_material[((size_t)ci * ny + cj) * nz + ck];
+                if (id0 >= su->n_materials) {
                     delete h;
-                    return fail_msg(MPB_EINVAL, "material id %d out of range", id);
+                    return fail_msg(MPB_EINVAL, "material id %d out of range", id0);
                 }
+                const uint8_t id = (uint8_t)remap[id0];
                 const int64_t f = (int64_t)j * F[2] + k;
                 ids[(size_t)(i * g.PP + f)] = id;
-                if (i < nx && j < ny && k < nz && su->materials[id].magnetic) {
+                if (i < nx && j < ny && k < nz && table[id].magnetic) {
                     cells.push_back(make_int2(i, (int)f));
                     mx0 = std::min(mx0, i);
                     mx1 = std::max(mx1, i + 1);
@@ -400,13 +429,13 @@ int mpb_create(const mpb_setup* su, mpb_handle** out) {
             chk(dev_alloc(h, &h->M[p][c], (size_t)(h->mplanes * g.PP)));
         }
     chk(dev_alloc(h, &h->ids, (size_t)h->nentries));
-    chk(dev_alloc(h, &h->mats, (size_t)su->n_materials));
+    chk(dev_alloc(h, &h->mats, (size_t)MPB_MAX_MATERIALS));
     chk(dev_alloc(h, &h->magcells, (size_t)h->nmag));
     chk(dev_alloc(h, &h->scratch, (size_t)h->nmag * 12));
     chk(dev_alloc(h, &h->st, 1));
     if (rc) { mpb_destroy(h); return rc; }
     CU(cudaMemcpy(h->ids, ids.data(), ids.size(), cudaMemcpyHostToDevice));
-    CU(cudaMemcpy(h->mats, su->materials, sizeof(mpb_material) * su->n_materials,
+    CU(cudaMemcpy(h->mats, table.data(), sizeof(mpb_material) * table.size(),
                   cudaMemcpyHostToDevice));
     if (h->nmag)
         CU(cudaMemcpy(h->magcells, cells.data(), sizeof(int2) * cells.size(),

@@ -107,10 +107,13 @@ __global__ void __launch_bounds__(256) k_hsweep(Geom g, Bufs b,
 // Split variant, kernel 2: E^{n+1} = ca (curl H - cb E) on every allocation
 // entry (em.py:206-232, 257-272).  Walls are applied afterwards.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void e_update_at(const Geom& g, const Bufs& b,
-                                            const mpb_material* __restrict__ mats,
-                                            const uint8_t* __restrict__ ids, int i,
-                                            int j, int k, int64_t o) {
+struct E3 { double x, y, z; };
+
+// Plain E^{n+1} at one entry (no walls), reading the new H from b.Hb.
+__device__ __forceinline__ E3 e_plain_at(const Geom& g, const Bufs& b,
+                                         const mpb_material* __restrict__ mats,
+                                         const uint8_t* __restrict__ ids, int i, int j, int k,
+                                         int64_t o) {
     const double* const* H = b.Hb;
     double cx = 0.0, cy = 0.0, cz = 0.0;
     const int64_t sx = g.PP, sy = g.F[2];
@@ -131,9 +134,23 @@ __device__ __forceinline__ void e_update_at(const Geom& g, const Bufs& b,
     }
     const uint8_t id = ids[o];
     const double ca = mats[id].ca, cb = mats[id].cb;
-    b.Eb[0][o] = ca * (cx - cb * b.Ea[0][o]);
-    b.Eb[1][o] = ca * (cy - cb * b.Ea[1][o]);
-    b.Eb[2][o] = ca * (cz - cb * b.Ea[2][o]);
+    E3 r;
+    r.x = ca * (cx - cb * b.Ea[0][o]);
+    r.y = ca * (cy - cb * b.Ea[1][o]);
+    r.z = ca * (cz - cb * b.Ea[2][o]);
+    return r;
+}
+
+// E^{n+1} = ca (curl H - cb E) on one allocation entry (em.py:206-232,
+// 257-272); walls are applied afterwards by k_wall.
+__device__ __forceinline__ void e_update_at(const Geom& g, const Bufs& b,
+                                            const mpb_material* __restrict__ mats,
+                                            const uint8_t* __restrict__ ids, int i,
+                                            int j, int k, int64_t o) {
+    const E3 r = e_plain_at(g, b, mats, ids, i, j, k, o);
+    b.Eb[0][o] = r.x;
+    b.Eb[1][o] = r.y;
+    b.Eb[2][o] = r.z;
 }
 
 __global__ void __launch_bounds__(256) k_esweep(Geom g, Bufs b,

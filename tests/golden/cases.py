@@ -121,6 +121,33 @@ CASES = {
         cfl=0.9, steps=400, llg=(1e-16, 1),
         probes=[("Ex", 0, 0, 20)],
     ),
+    # magnet spanning the full z extent (touches both z walls, MUR1) under a
+    # strong drive: deferred E recompute through z-wall rows
+    "zwall_magnet": dict(
+        grid=(8, 7, 6, 6e-6, 7e-6, 5e-6),
+        background=(0.0, 2.0),
+        boxes=[dict(box=(3, 6, 2, 5, 0, 6), eps_r=15.0, Ms=1.3926e5, alpha=2e-3,
+                    bias=900.0 * OE, bias_direction=(1, 0, 1))],
+        source=dict(f0=60e9, Tp=0.8e-12, amplitude=1e8, location=(2, 3, 1),
+                    polarization=(0.6, 0.0, 0.8)),
+        boundaries=dict(x0="PEC", x1="MUR1", y0="PMC", y1="MUR1", z0="MUR1",
+                        z1="MUR1"),
+        cfl=0.9, steps=150,
+        probes=[("Ex", 4, 3, 0), ("Ey", 4, 3, 6), ("Mz", 4, 3, 0), ("Hx", 4, 3, 5)],
+    ),
+    # thinnest grid: ny = nz = 2, all MUR1 (z-wall inner rows coincide)
+    "thin": dict(
+        grid=(6, 2, 2, 4e-6, 4e-6, 4e-6),
+        background=(0.0, 1.0),
+        boxes=[dict(box=(2, 4, 0, 2, 0, 2), eps_r=15.0, Ms=9.7e5, alpha=5e-3,
+                    bias=1500.0 * OE, bias_direction=(0, 0, 1))],
+        source=dict(f0=80e9, Tp=0.5e-12, amplitude=1e7, location=(1, 1, 1),
+                    polarization=(1.0, 0.0, 0.0)),
+        boundaries=dict(x0="MUR1", x1="MUR1", y0="MUR1", y1="MUR1", z0="MUR1",
+                        z1="MUR1"),
+        cfl=0.9, steps=200,
+        probes=[("Ex", 1, 1, 1), ("Ey", 3, 0, 0), ("My", 2, 1, 1)],
+    ),
     # bias override through run(bias=...) along a tilted sweep direction
     "bias3d": dict(
         grid=(8, 9, 10, 6e-6, 6e-6, 6e-6),
