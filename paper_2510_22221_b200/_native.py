@@ -63,7 +63,7 @@ def load_library(path: os.PathLike | None = None) -> C.CDLL:
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    p = Path(path) if path else Path(os.environ.get("MAGPHON_LIB", LIB_PATH))
     if not p.exists():
         raise RuntimeError(
             f"magphon_b200 CUDA library not built ({p}); run "

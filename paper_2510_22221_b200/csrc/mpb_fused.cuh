@@ -7,9 +7,7 @@ namespace {
 
 struct FusedState {
     SweepCfg sc{};
-    int NT = 512;
     int V = 2;
-    int MH = 2;
     int grid = 0;
     size_t smem = 0;
     int2* defer = nullptr;
@@ -20,23 +18,11 @@ struct FusedState {
 
 FusedState* fused_of(mpb_handle* h) { return reinterpret_cast<FusedState*>(h->fused); }
 
-template <int NT, int V, int MH>
+template <int V>
 int set_smem_attr(size_t smem) {
-    CU(cudaFuncSetAttribute(k_sweep<NT, V, MH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CU(cudaFuncSetAttribute(k_sweep<V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)smem));
     return MPB_OK;
-}
-
-// (threads, V, MH) instantiations: owned entries / H-phase entries per thread.
-#define MPB_SWEEP_VARIANTS(X)                                                    \
-    X(512, 1, 1) X(512, 1, 2) X(512, 1, 3) X(512, 2, 2) X(512, 2, 3) X(512, 2, 4) \
-    X(256, 4, 4) X(256, 4, 5) X(384, 3, 3) X(384, 3, 4)
-
-int sweep_attr(int NT, int V, int MH, size_t smem) {
-#define X(t, a, b) if (NT == t && V == a && MH == b) return set_smem_attr<t, a, b>(smem);
-    MPB_SWEEP_VARIANTS(X)
-#undef X
-    return fail_msg(MPB_EINVAL, "no sweep instantiation for NT=%d V=%d MH=%d", NT, V, MH);
 }
 
 int prepare_fused(mpb_handle* h, const Geom& g) {
@@ -56,61 +42,37 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
                         g.FyFz);
     sc.fz_magic = (uint32_t)(((1ull << 32) + Fz - 1) / Fz);
     if (Fz == 1) sc.fz_magic = 0;   // j = f for Fz == 1 handled below
-    // entries per CTA per plane: V per thread; the tile is shortened by the
-    // halo so that tile + halo row = V * threads (balanced H phase)
-    // large planes: 256 threads x 4 entries (no register spills at 1 CTA/SM);
-    // small planes: 512 x 1 for more CTAs
-    fs->NT = 512;
-    fs->V = 1;
-    if (g.FyFz >= 1024 * 64) { fs->NT = 256; fs->V = 4; }
-    if (const char* e = getenv("MPB_SWEEP_NT")) {   // 256 -> V=4, 384 -> V=3, 512 -> V=2
-        const int nt = atoi(e);
-        if (fs->V > 1 && (nt == 256 || nt == 384 || nt == 512)) {
-            fs->NT = nt;
-            fs->V = nt == 256 ? 4 : (nt == 384 ? 3 : 2);
-        }
-    }
-    sc.T = fs->V * fs->NT;
-    if (sc.hl > 0 && sc.hl <= sc.T / 2) sc.T -= sc.hl;
-    // tuning overrides for experiments (MPB_SWEEP_T, MPB_SWEEP_SLOTS, MPB_SWEEP_WAVES)
-    if (const char* e = getenv("MPB_SWEEP_T")) {
-        const int t = atoi(e);
-        if (t > 0 && t <= fs->V * fs->NT) sc.T = t;
-    }
-    fs->MH = (sc.T + sc.hl + fs->NT - 1) / fs->NT;
-    if (fs->MH > fs->V + 2)
-        return fail_msg(MPB_EINVAL, "z extent %d too large for the fused sweep", Fz);
+    // entries per CTA per plane: 2 per thread unless the plane is small
+    fs->V = g.FyFz >= 8 * kSweepThreads * sms ? 4 : (g.FyFz >= 2 * kSweepThreads * 64 ? 2 : 1);
+    sc.T = fs->V * kSweepThreads;
     sc.tiles = (g.FyFz + sc.T - 1) / sc.T;
-    bool fastdiv = true;
-    for (int a = 0; a < 3; ++a)
-        if (g.act[a] && !(g.d[a] >= 0x1p-40 && g.d[a] <= 0x1p10)) fastdiv = false;
-    sc.fastdiv = fastdiv ? 1 : 0;
+    {
+        bool fastdiv = true;
+        for (int a = 0; a < 3; ++a)
+            if (g.act[a] && !(g.d[a] >= 0x1p-40 && g.d[a] <= 0x1p10)) fastdiv = false;
+        sc.fastdiv = fastdiv ? 1 : 0;
+    }
     sc.ecap = (sc.T + sc.hl + sc.eh + 4 + 1) & ~1;
     sc.hcap = (sc.T + sc.hl + 4 + 1) & ~1;
     sc.icap = sc.T + sc.hl + 48;
     sc.stage_bytes = ((3 * sc.ecap + 3 * sc.hcap) * 8 + sc.icap + 127) / 128 * 128;
     sc.ring_offset = ((g.max_iters + 2) * 8 + 127) / 128 * 128;
+    fs->smem = (size_t)sc.ring_offset + (size_t)kSlots * sc.stage_bytes;
+    if (const char* e = getenv("MPB_SWEEP_WAVES")) (void)e;
     const size_t static_smem = 8 * 1024;
-    sc.slots = kMaxSlots;
-    if (const char* e = getenv("MPB_SWEEP_SLOTS")) sc.slots = std::max(3, std::min(kMaxSlots, atoi(e)));
-    while (sc.slots > 3 && (size_t)sc.ring_offset + (size_t)sc.slots * sc.stage_bytes +
-                                   static_smem > (size_t)smem_optin)
-        --sc.slots;
-    fs->smem = (size_t)sc.ring_offset + (size_t)sc.slots * sc.stage_bytes;
     if (fs->smem + static_smem > (size_t)smem_optin)
         return fail_msg(MPB_EINVAL, "fused sweep staging (%zu B) exceeds shared memory",
                         fs->smem);
     // x-chunks: ~8 waves of one CTA per SM, chunks of >= 24 planes
     const int Fx = g.F[0];
-    int waves = 8;
-    if (const char* e = getenv("MPB_SWEEP_WAVES")) waves = std::max(1, atoi(e));
-    const int want = std::max(1, (waves * sms + sc.tiles - 1) / sc.tiles);
+    const int want = std::max(1, (8 * sms + sc.tiles - 1) / sc.tiles);
     const int maxch = std::max(1, Fx / 24);
     sc.nchunks = std::max(1, std::min(want, maxch));
     sc.chunk = (Fx + sc.nchunks - 1) / sc.nchunks;
     sc.nchunks = (Fx + sc.chunk - 1) / sc.chunk;
     fs->grid = sc.tiles * sc.nchunks;
-    int rc = sweep_attr(fs->NT, fs->V, fs->MH, fs->smem);
+    int rc = fs->V == 4 ? set_smem_attr<4>(fs->smem)
+                        : (fs->V == 2 ? set_smem_attr<2>(fs->smem) : set_smem_attr<1>(fs->smem));
     if (rc) return rc;
     // deferred E entries: {c, c+x, c+y, c+z} over magnetic cells
     std::vector<int64_t> keys;
@@ -180,15 +142,12 @@ void destroy_fused(mpb_handle* h) {
 
 int launch_fused(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s) {
     FusedState* fs = fused_of(h);
-#define X(t, a, c)                                                                    \
-    if (fs->NT == t && fs->V == a && fs->MH == c) {                                   \
-        k_sweep<t, a, c><<<fs->grid, t, fs->smem, s>>>(g, b, h->mats, h->ids, h->st, \
-                                                      fs->sc);                        \
-        return MPB_OK;                                                                \
+    switch (fs->V) {
+        case 4: k_sweep<4><<<fs->grid, kSweepThreads, fs->smem, s>>>(g, b, h->mats, h->ids, h->st, fs->sc); break;
+        case 2: k_sweep<2><<<fs->grid, kSweepThreads, fs->smem, s>>>(g, b, h->mats, h->ids, h->st, fs->sc); break;
+        default: k_sweep<1><<<fs->grid, kSweepThreads, fs->smem, s>>>(g, b, h->mats, h->ids, h->st, fs->sc); break;
     }
-    MPB_SWEEP_VARIANTS(X)
-#undef X
-    return fail_msg(MPB_EINVAL, "no sweep instantiation");
+    return MPB_OK;
 }
 
 int launch_deferred(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s) {

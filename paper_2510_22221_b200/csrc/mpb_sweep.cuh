@@ -85,11 +85,10 @@ struct SweepCfg {
     int ring_offset;    // bytes of dynamic smem before the ring (LLG history)
     int nmat;           // entries of the material table
     int fastdiv;        // spacings within [2^-40, 2^10]: range-guarded divisions
-    int slots;          // ring depth (3 or 4)
 };
 
-constexpr int kMagneticIdBit = 0x80;   // material ids >= 128 are magnetic
-constexpr int kMaxSlots = 4;
+constexpr int kSweepThreads = 512;
+constexpr int kSlots = 3;
 
 __device__ __forceinline__ int fz_div(uint32_t f, uint32_t magic) {
     return magic ? (int)__umulhi(f, magic) : (int)f;   // magic 0 <=> Fz == 1
@@ -132,76 +131,65 @@ __device__ __noinline__ int llg_cell_local(const mpb_material* __restrict__ mats
     return rc;
 }
 
-// Per-thread entry descriptors.  A thread owns the same (j,k) entries on
-// every plane of its x-march, so indices, ghost predicates and store masks
-// are computed once before the march.
-enum : unsigned {
-    kJ0 = 1u, kJN = 2u, kK0 = 4u, kKN = 8u,      // j==0, j==ny, k==0, k==nz
-    kVX = 16u, kVKZ = 32u, kVJY = 64u,           // Hx valid (j<ny&&k<nz), k<nz, j<ny
-    kLIVE = 128u, kOWN = 256u,
-    kK1 = 512u, kKNm1 = 1024u,                   // k==1, k==nz-1 (z-wall inner rows)
-    kXLINE = 2048u                               // Ex z-wall deferred (j<=1 || j>=ny-1)
+// H^{n+1} at one entry of the staged plane (in place in shared memory).
+// Straight-line: all six differences and divisions are issued back to back
+// and the division guard is checked once for the batch.
+struct HCtx {
+    const double* Ex; const double* Ey; const double* Ez;
+    const double* Ey1; const double* Ez1;
+    double* Hx; double* Hy; double* Hz;
 };
 
-struct EntryIdx {
-    int e;        // shared-memory index of the entry (relative to a0)
-    int ejm;      // index of (j-1) neighbour (clamped to e when j == 0)
-    int ekm;      // index of (k-1) neighbour (clamped to e when k == 0)
-    int f;        // flat index in the plane
-    unsigned fl;  // flags above
-};
-
-__device__ __forceinline__ EntryIdx make_entry(int f, int f_end, int own_from, int a0,
-                                               int Fz, uint32_t magic, int ny, int nz,
-                                               bool ay) {
-    EntryIdx x;
-    x.f = f;
-    x.e = f - a0;
-    x.fl = 0;
-    if (f < f_end) {
-        const int j = fz_div((uint32_t)f, magic);
-        const int k = f - j * Fz;
-        x.fl |= kLIVE;
-        if (f >= own_from) x.fl |= kOWN;
-        if (j == 0) x.fl |= kJ0;
-        if (j == ny) x.fl |= kJN;
-        if (k == 0) x.fl |= kK0;
-        if (k == nz) x.fl |= kKN;
-        if (j < ny && k < nz) x.fl |= kVX;
-        if (k < nz) x.fl |= kVKZ;
-        if (j < ny) x.fl |= kVJY;
-        if (k == 1) x.fl |= kK1;
-        if (k == nz - 1) x.fl |= kKNm1;
-        if (ay && (j <= 1 || j >= ny - 1)) x.fl |= kXLINE;
-        x.ejm = j > 0 ? x.e - Fz : x.e;
-        x.ekm = k > 0 ? x.e - 1 : x.e;
-    } else {
-        x.ejm = x.ekm = x.e = 0;
+__device__ __forceinline__ void h_entry(const Geom& g, const HCtx& c, int e, int j, int k,
+                                        bool cellplane, int Fz, double ry, double rz,
+                                        double rx, double& cx, double& cy, double& cz,
+                                        bool& vx, bool& vy, bool& vz, bool g_fastdiv) {
+    vx = j < g.n[1] && k < g.n[2];
+    vy = cellplane && k < g.n[2];
+    vz = cellplane && j < g.n[1];
+    const double ex = c.Ex[e], ey = c.Ey[e], ez = c.Ez[e];
+    const double a0 = c.Ez[e + Fz] - ez;   // dEz/dy
+    const double a1 = c.Ex[e + Fz] - ex;   // dEx/dy
+    const double a2 = c.Ey[e + 1] - ey;    // dEy/dz
+    const double a3 = c.Ex[e + 1] - ex;    // dEx/dz
+    const double a4 = c.Ez1[e] - ez;       // dEz/dx
+    const double a5 = c.Ey1[e] - ey;       // dEy/dx
+    // range guard per component group, masked by validity (padding entries
+    // and collapsed axes never send an entry to the slow path)
+    unsigned gX = 0, gY = 0, gZ = 0;
+    double q0 = qdiv(a0, g.d[1], ry, gX);   // -> cEx
+    double q1 = qdiv(a1, g.d[1], ry, gZ);   // -> cEz
+    double q2 = qdiv(a2, g.d[2], rz, gX);   // -> cEx
+    double q3 = qdiv(a3, g.d[2], rz, gY);   // -> cEy
+    double q4 = qdiv(a4, g.d[0], rx, gY);   // -> cEy
+    double q5 = qdiv(a5, g.d[0], rx, gZ);   // -> cEz
+    const bool bad = !g_fastdiv || (vx && gX > kGuardSpan) || (vy && gY > kGuardSpan) ||
+                     (vz && gZ > kGuardSpan);
+    if (__builtin_expect(bad, 0)) {
+        q0 = xdiv(a0, g.d[1], ry); q1 = xdiv(a1, g.d[1], ry);
+        q2 = xdiv(a2, g.d[2], rz); q3 = xdiv(a3, g.d[2], rz);
+        q4 = xdiv(a4, g.d[0], rx); q5 = xdiv(a5, g.d[0], rx);
     }
-    return x;
+    // em.py:130-138 accumulation order, collapsed axes omitted
+    cx = 0.0; cy = 0.0; cz = 0.0;
+    if (g.act[1]) { cx = cx + q0; cz = cz - q1; }
+    if (g.act[2]) { cx = cx - q2; cy = cy + q3; }
+    if (g.act[0]) { cy = cy - q4; cz = cz + q5; }
 }
 
-// Ghost-aware backward-difference numerators of curl H at one E entry
-// (em.py:185-203): "hi - lo" per term, PMC ghosts = -edge, other walls 0.
-struct ENum { double b0, b1, b2, b3, b4, b5; };
-
-template <int NT, int V, int MH>
-__global__ void __launch_bounds__(NT, 1)
+template <int V>
+__global__ void __launch_bounds__(kSweepThreads, 1)
 k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
         const uint8_t* __restrict__ gids, StepState* st, SweepCfg sc) {
-    extern __shared__ __align__(128) double smem_d[];
-    __shared__ uint64_t bars[kMaxSlots];
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ uint64_t bars[kSlots];
     __shared__ int s_rc[2];
     __shared__ int s_anymag;
-    __shared__ double2 s_cacb[MPB_MAX_MATERIALS];
+    __shared__ double s_cacb[MPB_MAX_MATERIALS * 2];
+    __shared__ unsigned char s_mag[MPB_MAX_MATERIALS];
     __shared__ double s_murz[MPB_MAX_MATERIALS];
-    unsigned long long* s_hist = reinterpret_cast<unsigned long long*>(smem_d);
-    unsigned char* smem_b = reinterpret_cast<unsigned char*>(smem_d);
-    const int ring0 = sc.ring_offset / 8;            // in doubles
-    const int sd = sc.stage_bytes / 8;               // doubles per slot
-    const int nslots = sc.slots;
-    // producer: the last thread -- it owns the fewest E entries (T < V*NT)
-    const int prod = NT - 1;
+    unsigned long long* s_hist = reinterpret_cast<unsigned long long*>(smem);
+    unsigned char* ring = smem + sc.ring_offset;
 
     if (st->fail) return;
     const int tid = threadIdx.x;
@@ -228,68 +216,61 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
     const uint32_t hbytes = (uint32_t)(ah - a0) * 8u;
     const uint32_t ibytes = (uint32_t)(iae - ia0);
 
-    for (int q = tid; q < sc.nmat; q += NT) {
-        s_cacb[q] = make_double2(mats[q].ca, mats[q].cb);
+    for (int q = tid; q < sc.nmat; q += blockDim.x) {
+        s_cacb[2 * q] = mats[q].ca;
+        s_cacb[2 * q + 1] = mats[q].cb;
+        s_mag[q] = (unsigned char)mats[q].magnetic;
         s_murz[q] = mats[q].mur_k[2];
     }
-    for (int r = tid; r <= g.max_iters + 1; r += NT) s_hist[r] = 0ull;
-    if (tid == prod) {
+    for (int r = tid; r <= g.max_iters + 1; r += blockDim.x) s_hist[r] = 0ull;
+    if (tid == 0) {
         s_rc[0] = 0x7fffffff; s_rc[1] = 0; s_anymag = 0;
-        for (int q = 0; q < nslots; ++q) mbar_init(&bars[q], 1);
+        for (int q = 0; q < kSlots; ++q) mbar_init(&bars[q], 1);
         mbar_fence_init();
     }
     __syncthreads();
 
-    // slot layout (doubles): E[3][ecap] | H[3][hcap] | ids (bytes)
-    auto slot = [&](int p) { return (p - pstart) % nslots; };
-    auto sbase = [&](int s) { return ring0 + s * sd; };
-    auto issue = [&](int p) {   // producer only
+    // slot layout: E[3][ecap] | H[3][hcap] | ids[icap]
+    auto slot = [&](int p) { return (p - pstart) % kSlots; };
+    auto sE = [&](int s, int c) {
+        return reinterpret_cast<double*>(ring + (size_t)s * sc.stage_bytes) + c * sc.ecap;
+    };
+    auto sH = [&](int s, int c) {
+        return reinterpret_cast<double*>(ring + (size_t)s * sc.stage_bytes) +
+               3 * sc.ecap + c * sc.hcap;
+    };
+    auto sI = [&](int s) {
+        return ring + (size_t)s * sc.stage_bytes + (3 * sc.ecap + 3 * sc.hcap) * 8;
+    };
+    auto issue = [&](int p) {   // thread 0 only
         const int s = slot(p);
         const bool full = p < i1;
         const uint32_t bytes = 3 * ebytes + (full ? 3 * hbytes + ibytes : 0u);
         mbar_expect_tx(&bars[s], bytes);
         const int64_t base = (int64_t)p * g.PP;
-        double* sb = smem_d + sbase(s);
-        for (int c = 0; c < 3; ++c)
-            tma_load_1d(sb + c * sc.ecap, b.Ea[c] + base + a0, ebytes, &bars[s]);
+        for (int c = 0; c < 3; ++c) tma_load_1d(sE(s, c), b.Ea[c] + base + a0, ebytes, &bars[s]);
         if (full) {
             for (int c = 0; c < 3; ++c)
-                tma_load_1d(sb + 3 * sc.ecap + c * sc.hcap, b.Ha[c] + base + a0, hbytes,
-                            &bars[s]);
-            tma_load_1d(sb + 3 * sc.ecap + 3 * sc.hcap, gids + base + ia0, ibytes, &bars[s]);
+                tma_load_1d(sH(s, c), b.Ha[c] + base + a0, hbytes, &bars[s]);
+            tma_load_1d(sI(s), gids + base + ia0, ibytes, &bars[s]);
         }
     };
-    if (tid == prod)
-        for (int p = pstart; p <= plast && p < pstart + nslots; ++p) issue(p);
+    if (tid == 0)
+        for (int p = pstart; p <= plast && p < pstart + kSlots; ++p) issue(p);
 
     const double ry = g.act[1] ? recip_of(g.d[1]) : 1.0;
     const double rz = g.act[2] ? recip_of(g.d[2]) : 1.0;
     const double rx = g.act[0] ? recip_of(g.d[0]) : 1.0;
-    const double dx = g.d[0], dy = g.d[1], dz = g.d[2];
-    const double coef = g.coef_h;
     const int Fz = g.F[2];
     const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
-    const bool ax = g.act[0], ay = g.act[1], az = g.act[2];
+    // collapsed axes: their (unused) quotients must not trip the guard
+    const bool fastdiv = sc.fastdiv != 0 && g.act[0] && g.act[1] && g.act[2];
+    const bool zw0 = g.act[2] && g.faces[4] != MPB_FACE_PMC;
+    const bool zw1 = g.act[2] && g.faces[5] != MPB_FACE_PMC;
+    const bool z0pec = g.faces[4] == MPB_FACE_PEC, z1pec = g.faces[5] == MPB_FACE_PEC;
     const bool pmc_x0 = g.faces[0] == MPB_FACE_PMC, pmc_x1 = g.faces[1] == MPB_FACE_PMC;
     const bool pmc_y0 = g.faces[2] == MPB_FACE_PMC, pmc_y1 = g.faces[3] == MPB_FACE_PMC;
     const bool pmc_z0 = g.faces[4] == MPB_FACE_PMC, pmc_z1 = g.faces[5] == MPB_FACE_PMC;
-    const bool guarded = sc.fastdiv != 0;
-    const bool zw0 = az && g.faces[4] != MPB_FACE_PMC, zw1 = az && g.faces[5] != MPB_FACE_PMC;
-    const bool z0pec = g.faces[4] == MPB_FACE_PEC, z1pec = g.faces[5] == MPB_FACE_PEC;
-    const uint32_t PP = (uint32_t)g.PP;              // element offsets fit 32 bits
-
-    EntryIdx he[MH], ee[V];
-    bool warp_interior[V];
-#pragma unroll
-    for (int m = 0; m < MH; ++m)
-        he[m] = make_entry(hlo + tid + m * NT, f1, f0, a0, Fz, sc.fz_magic, ny, nz, ay);
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-        ee[v] = make_entry(f0 + tid + v * NT, f1, f0, a0, Fz, sc.fz_magic, ny, nz, ay);
-        const bool inner = !(ee[v].fl & (kJ0 | kJN | kK0 | kKN)) || !(ee[v].fl & kLIVE);
-        warp_interior[v] = __all_sync(0xffffffffu, inner);
-    }
-    const int iofs = a0 - ia0;   // ids index = e + iofs
 
     double hy_prev[V], hz_prev[V];
 #pragma unroll
@@ -297,71 +278,46 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
 
     for (int p = pstart; p <= i1 - 1; ++p) {
         const int s = slot(p);
-        const bool xnext = ax && p < nx;                 // plane p+1 used by dx terms
+        const bool xnext = g.act[0] && p < nx;           // plane p+1 used by dx terms
         const int s1 = slot(p + 1);
-        if (tid == prod) {
-            mbar_wait(&bars[s], ((p - pstart) / nslots) & 1);
-            if (xnext) mbar_wait(&bars[s1], ((p + 1 - pstart) / nslots) & 1);
+        if (tid == 0) {
+            mbar_wait(&bars[s], ((p - pstart) / kSlots) & 1);
+            if (xnext) mbar_wait(&bars[s1], ((p + 1 - pstart) / kSlots) & 1);
         }
         __syncthreads();   // staged data visible; E phase of p-1 done everywhere
-        if (tid == prod && p > pstart && p + nslots - 1 <= plast) {
+        if (tid == 0 && p > pstart && p + 2 <= plast) {
             fence_proxy_async();
-            issue(p + nslots - 1);  // into the slot plane p-1 just released
+            issue(p + 2);  // into the slot plane p-1 just released
         }
-        const int bE = sbase(s);
-        const int bEx = bE, bEy = bE + sc.ecap, bEz = bE + 2 * sc.ecap;
-        const int bEy1 = sbase(s1) + sc.ecap, bEz1 = sbase(s1) + 2 * sc.ecap;
-        const int bHx = bE + 3 * sc.ecap, bHy = bHx + sc.hcap, bHz = bHy + sc.hcap;
-        const unsigned char* ids = smem_b + (size_t)(bE + 3 * sc.ecap + 3 * sc.hcap) * 8;
+        HCtx hc{sE(s, 0), sE(s, 1), sE(s, 2), sE(s1, 1), sE(s1, 2),
+                sH(s, 0), sH(s, 1), sH(s, 2)};
+        const unsigned char* ids = sI(s);
         const bool emit = p >= i0;
-        const bool cellplane = p < nx || !ax;
+        const bool cellplane = p < nx || !g.act[0];
 
-        // ---- H^{n+1}(p, g) on [hlo, f1), in place (em.py:117-182) -----------
-#pragma unroll
-        for (int m = 0; m < MH; ++m) {
-            const EntryIdx& x = he[m];
-            if (!(x.fl & kLIVE)) continue;
-            const int e = x.e;
-            const double ex = smem_d[bEx + e], ey = smem_d[bEy + e], ez = smem_d[bEz + e];
-            const double a0v = smem_d[bEz + e + Fz] - ez;   // dEz/dy
-            const double a1v = smem_d[bEx + e + Fz] - ex;   // dEx/dy
-            const double a2v = smem_d[bEy + e + 1] - ey;    // dEy/dz
-            const double a3v = smem_d[bEx + e + 1] - ex;    // dEx/dz
-            const double a4v = smem_d[bEz1 + e] - ez;       // dEz/dx
-            const double a5v = smem_d[bEy1 + e] - ey;       // dEy/dx
-            unsigned gy = 0, gz = 0, gx = 0;
-            double q0 = qdiv(a0v, dy, ry, gy), q1 = qdiv(a1v, dy, ry, gy);
-            double q2 = qdiv(a2v, dz, rz, gz), q3 = qdiv(a3v, dz, rz, gz);
-            double q4 = qdiv(a4v, dx, rx, gx), q5 = qdiv(a5v, dx, rx, gx);
-            const bool vx = x.fl & kVX;
-            const bool vy = cellplane && (x.fl & kVKZ);
-            const bool vz = cellplane && (x.fl & kVJY);
-            const bool bad = !guarded || (ay && gy > kGuardSpan) || (az && gz > kGuardSpan) ||
-                             (ax && gx > kGuardSpan);
-            if (__builtin_expect(bad, 0)) {
-                q0 = xdiv(a0v, dy, ry); q1 = xdiv(a1v, dy, ry);
-                q2 = xdiv(a2v, dz, rz); q3 = xdiv(a3v, dz, rz);
-                q4 = xdiv(a4v, dx, rx); q5 = xdiv(a5v, dx, rx);
-            }
-            double cx = 0.0, cy = 0.0, cz = 0.0;            // em.py:130-138 order
-            if (ay) { cx = cx + q0; cz = cz - q1; }
-            if (az) { cx = cx - q2; cy = cy + q3; }
-            if (ax) { cy = cy - q4; cz = cz + q5; }
-            const int id = ids[e + iofs];
-            const bool magnetic = cellplane && vx && (id & kMagneticIdBit);
+        // ---- H^{n+1}(p, g) for g in [hlo, f1), in place --------------------
+        for (int gg = hlo + tid; gg < f1; gg += kSweepThreads) {
+            const int j = fz_div((uint32_t)gg, sc.fz_magic);
+            const int k = gg - j * Fz;
+            const int e = gg - a0;
+            double cx, cy, cz;
+            bool vx, vy, vz;
+            h_entry(g, hc, e, j, k, cellplane, Fz, ry, rz, rx, cx, cy, cz, vx, vy, vz, fastdiv);
+            const int id = ids[gg - ia0];
+            const bool magnetic = cellplane && j < ny && k < nz && s_mag[id];
             if (__builtin_expect(!magnetic, 1)) {
-                if (vx) smem_d[bHx + e] = smem_d[bHx + e] - coef * cx;
-                if (vy) smem_d[bHy + e] = smem_d[bHy + e] - coef * cy;
-                if (vz) smem_d[bHz + e] = smem_d[bHz + e] - coef * cz;
+                if (vx) hc.Hx[e] = hc.Hx[e] - g.coef_h * cx;
+                if (vy) hc.Hy[e] = hc.Hy[e] - g.coef_h * cy;
+                if (vz) hc.Hz[e] = hc.Hz[e] - g.coef_h * cz;
             } else {
-                const int64_t om = (int64_t)(p - g.mx0) * g.PP + x.f;
-                const double hn[3] = {smem_d[bHx + e], smem_d[bHy + e], smem_d[bHz + e]};
+                const int64_t om = (int64_t)(p - g.mx0) * g.PP + gg;
+                const double hn[3] = {hc.Hx[e], hc.Hy[e], hc.Hz[e]};
                 const double mn[3] = {b.Ma[0][om], b.Ma[1][om], b.Ma[2][om]};
                 const double ce[3] = {cx, cy, cz};
                 double ho[3], mo[3];
-                const bool own = emit && (x.fl & kOWN);
+                const bool own = emit && gg >= f0;
                 const int rc = llg_cell_local(mats, id, &g, hn, mn, ce, ho, mo, s_hist, own);
-                smem_d[bHx + e] = ho[0]; smem_d[bHy + e] = ho[1]; smem_d[bHz + e] = ho[2];
+                hc.Hx[e] = ho[0]; hc.Hy[e] = ho[1]; hc.Hz[e] = ho[2];
                 if (own) {
                     b.Mb[0][om] = mo[0]; b.Mb[1][om] = mo[1]; b.Mb[2][om] = mo[2];
                     atomicMin(&s_rc[0], rc);
@@ -372,94 +328,96 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
         }
         __syncthreads();
 
-        // ---- E^{n+1}(p, f) for the owned range (em.py:206-272) -------------
-        const uint32_t base = (uint32_t)p * PP;
-        const bool xedge = p == 0 || p == nx;            // plane-uniform
-        const bool exEy = ax && (p <= 1 || p >= nx - 1); // Ey z-wall deferred to k_zfix
+        // ---- E^{n+1}(p, f) for the owned range ------------------------------
+        const double* Hx = hc.Hx;
+        const double* Hy = hc.Hy;
+        const double* Hz = hc.Hz;
+        const int64_t base = (int64_t)p * g.PP;
 #pragma unroll
         for (int v = 0; v < V; ++v) {
-            const EntryIdx& x = ee[v];
-            if (!(x.fl & kLIVE)) continue;
-            const int e = x.e;
-            const double hx = smem_d[bHx + e], hy = smem_d[bHy + e], hz = smem_d[bHz + e];
-            if (emit) {
-                const double hz_jm = smem_d[bHz + x.ejm], hx_jm = smem_d[bHx + x.ejm];
-                const double hy_km = smem_d[bHy + x.ekm], hx_km = smem_d[bHx + x.ekm];
-                double b0, b1, b2, b3, b4, b5;
-                if (warp_interior[v] && !xedge) {
-                    b0 = hz - hz_jm; b1 = hx - hx_jm; b2 = hy - hy_km;
-                    b3 = hx - hx_km; b4 = hz - hz_prev[v]; b5 = hy - hy_prev[v];
-                } else {
+            const int f = f0 + tid + v * kSweepThreads;
+            if (f < f1) {
+                const int e = f - a0;
+                const double hx = Hx[e], hy = Hy[e], hz = Hz[e];
+                if (emit) {
+                    const int j = fz_div((uint32_t)f, sc.fz_magic);
+                    const int k = f - j * Fz;
+                    const int ejm = j > 0 ? e - Fz : e;   // clamp: never read off-range
+                    const int ekm = k > 0 ? e - 1 : e;
+                    const double hz_jm = Hz[ejm], hx_jm = Hx[ejm];
+                    const double hy_km = Hy[ekm], hx_km = Hx[ekm];
                     // backward differences with PMC ghosts (em.py:185-203)
-                    const bool j0 = x.fl & kJ0, jn = x.fl & kJN, k0 = x.fl & kK0,
-                               kn = x.fl & kKN;
-                    const double zhi = jn ? (pmc_y1 ? -hz_jm : 0.0) : hz;
-                    const double zlo = j0 ? (pmc_y0 ? -hz : 0.0) : hz_jm;
-                    const double xhi_j = jn ? (pmc_y1 ? -hx_jm : 0.0) : hx;
-                    const double xlo_j = j0 ? (pmc_y0 ? -hx : 0.0) : hx_jm;
-                    const double yhi_k = kn ? (pmc_z1 ? -hy_km : 0.0) : hy;
-                    const double ylo_k = k0 ? (pmc_z0 ? -hy : 0.0) : hy_km;
-                    const double xhi_k = kn ? (pmc_z1 ? -hx_km : 0.0) : hx;
-                    const double xlo_k = k0 ? (pmc_z0 ? -hx : 0.0) : hx_km;
-                    const bool xl = p == 0, xh = p == nx;
-                    const double zhi_i = xh ? (pmc_x1 ? -hz_prev[v] : 0.0) : hz;
-                    const double zlo_i = xl ? (pmc_x0 ? -hz : 0.0) : hz_prev[v];
-                    const double yhi_i = xh ? (pmc_x1 ? -hy_prev[v] : 0.0) : hy;
-                    const double ylo_i = xl ? (pmc_x0 ? -hy : 0.0) : hy_prev[v];
-                    b0 = zhi - zlo; b1 = xhi_j - xlo_j; b2 = yhi_k - ylo_k;
-                    b3 = xhi_k - xlo_k; b4 = zhi_i - zlo_i; b5 = yhi_i - ylo_i;
+                    const double zhi = (j == ny) ? (pmc_y1 ? -hz_jm : 0.0) : hz;
+                    const double zlo = (j == 0) ? (pmc_y0 ? -hz : 0.0) : hz_jm;
+                    const double xhi = (j == ny) ? (pmc_y1 ? -hx_jm : 0.0) : hx;
+                    const double xlo = (j == 0) ? (pmc_y0 ? -hx : 0.0) : hx_jm;
+                    const double yhi_k = (k == nz) ? (pmc_z1 ? -hy_km : 0.0) : hy;
+                    const double ylo_k = (k == 0) ? (pmc_z0 ? -hy : 0.0) : hy_km;
+                    const double xhi_k = (k == nz) ? (pmc_z1 ? -hx_km : 0.0) : hx;
+                    const double xlo_k = (k == 0) ? (pmc_z0 ? -hx : 0.0) : hx_km;
+                    const double zhi_i = (p == nx) ? (pmc_x1 ? -hz_prev[v] : 0.0) : hz;
+                    const double zlo_i = (p == 0) ? (pmc_x0 ? -hz : 0.0) : hz_prev[v];
+                    const double yhi_i = (p == nx) ? (pmc_x1 ? -hy_prev[v] : 0.0) : hy;
+                    const double ylo_i = (p == 0) ? (pmc_x0 ? -hy : 0.0) : hy_prev[v];
+                    const double b0 = zhi - zlo, b1 = xhi - xlo, b2 = yhi_k - ylo_k;
+                    const double b3 = xhi_k - xlo_k, b4 = zhi_i - zlo_i, b5 = yhi_i - ylo_i;
+                    unsigned gg2 = 0;
+                    double q0 = qdiv(b0, g.d[1], ry, gg2), q1 = qdiv(b1, g.d[1], ry, gg2);
+                    double q2 = qdiv(b2, g.d[2], rz, gg2), q3 = qdiv(b3, g.d[2], rz, gg2);
+                    double q4 = qdiv(b4, g.d[0], rx, gg2), q5 = qdiv(b5, g.d[0], rx, gg2);
+                    if (__builtin_expect(!fastdiv || gg2 > kGuardSpan, 0)) {
+                        q0 = xdiv(b0, g.d[1], ry); q1 = xdiv(b1, g.d[1], ry);
+                        q2 = xdiv(b2, g.d[2], rz); q3 = xdiv(b3, g.d[2], rz);
+                        q4 = xdiv(b4, g.d[0], rx); q5 = xdiv(b5, g.d[0], rx);
+                    }
+                    double cx = 0.0, cy = 0.0, cz = 0.0;   // em.py:217-231 order
+                    if (g.act[1]) { cx = cx + q0; cz = cz - q1; }
+                    if (g.act[2]) { cx = cx - q2; cy = cy + q3; }
+                    if (g.act[0]) { cy = cy - q4; cz = cz + q5; }
+                    const int id = ids[f - ia0];
+                    const double ca = s_cacb[2 * id], cb = s_cacb[2 * id + 1];
+                    const double* Ex = hc.Ex;
+                    const double* Ey = hc.Ey;
+                    const double* Ez = hc.Ez;
+                    const double exa = Ex[e], eya = Ey[e];
+                    const double w0 = ca * (cx - cb * exa);
+                    const double w1 = ca * (cy - cb * eya);
+                    const double w2 = ca * (cz - cb * Ez[e]);
+                    const uint32_t o = (uint32_t)base + (uint32_t)f;
+                    // z walls (em.py:336-359) in the sweep: the owner of the inner
+                    // entry (k=1 / k=nz-1) writes the tangential wall value; lines
+                    // an x/y wall reads or writes are left to k_zfix (run after the
+                    // x/y wall kernels, preserving the face order x0..z1)
+                    const bool zx = !(g.act[1] && (j <= 1 || j >= ny - 1));
+                    const bool zy = !(g.act[0] && (p <= 1 || p >= nx - 1));
+                    bool wx = true, wy = true;
+                    if ((zw0 && k == 0) || (zw1 && k == nz)) { wx = !zx; wy = !zy; }
+                    if (wx) b.Eb[0][o] = w0;
+                    if (wy) b.Eb[1][o] = w1;
+                    b.Eb[2][o] = w2;
+                    if (zw0 && k == 1) {
+                        const double kk = s_murz[ids[f - 1 - ia0]];
+                        if (zx) b.Eb[0][o - 1] = z0pec ? 0.0 : exa + kk * (w0 - Ex[e - 1]);
+                        if (zy) b.Eb[1][o - 1] = z0pec ? 0.0 : eya + kk * (w1 - Ey[e - 1]);
+                    }
+                    if (zw1 && k == nz - 1) {
+                        const double kk = s_murz[ids[f + 1 - ia0]];
+                        if (zx) b.Eb[0][o + 1] = z1pec ? 0.0 : exa + kk * (w0 - Ex[e + 1]);
+                        if (zy) b.Eb[1][o + 1] = z1pec ? 0.0 : eya + kk * (w1 - Ey[e + 1]);
+                    }
+                    const bool cp = p < nx || !g.act[0];
+                    if (j < ny && k < nz) b.Hb[0][o] = hx;
+                    if (cp && k < nz) b.Hb[1][o] = hy;
+                    if (cp && j < ny) b.Hb[2][o] = hz;
                 }
-                unsigned gy = 0, gz = 0, gx = 0;
-                double q0 = qdiv(b0, dy, ry, gy), q1 = qdiv(b1, dy, ry, gy);
-                double q2 = qdiv(b2, dz, rz, gz), q3 = qdiv(b3, dz, rz, gz);
-                double q4 = qdiv(b4, dx, rx, gx), q5 = qdiv(b5, dx, rx, gx);
-                const bool bad = !guarded || (ay && gy > kGuardSpan) ||
-                                 (az && gz > kGuardSpan) || (ax && gx > kGuardSpan);
-                if (__builtin_expect(bad, 0)) {
-                    q0 = xdiv(b0, dy, ry); q1 = xdiv(b1, dy, ry);
-                    q2 = xdiv(b2, dz, rz); q3 = xdiv(b3, dz, rz);
-                    q4 = xdiv(b4, dx, rx); q5 = xdiv(b5, dx, rx);
-                }
-                double cx = 0.0, cy = 0.0, cz = 0.0;   // em.py:217-231 order
-                if (ay) { cx = cx + q0; cz = cz - q1; }
-                if (az) { cx = cx - q2; cy = cy + q3; }
-                if (ax) { cy = cy - q4; cz = cz + q5; }
-                const double2 cc = s_cacb[ids[e + iofs]];
-                const uint32_t o = base + (uint32_t)x.f;
-                const double exa = smem_d[bEx + e], eya = smem_d[bEy + e];
-                const double w0 = cc.x * (cx - cc.y * exa);
-                const double w1 = cc.x * (cy - cc.y * eya);
-                const double w2 = cc.x * (cz - cc.y * smem_d[bEz + e]);
-                // z walls (em.py:336-359) applied in the sweep: the owner of the
-                // inner entry (k=1 / k=nz-1) writes the tangential wall value;
-                // lines an x/y wall touches are left to k_zfix (after x/y walls)
-                const bool zx = !(x.fl & kXLINE), zy = !exEy;
-                bool wx = true, wy = true;
-                if ((zw0 && (x.fl & kK0)) || (zw1 && (x.fl & kKN))) { wx = !zx; wy = !zy; }
-                if (wx) b.Eb[0][o] = w0;
-                if (wy) b.Eb[1][o] = w1;
-                b.Eb[2][o] = w2;
-                if (zw0 && (x.fl & kK1)) {
-                    const double kk = s_murz[ids[e - 1 + iofs]];
-                    if (zx) b.Eb[0][o - 1] = z0pec ? 0.0 : exa + kk * (w0 - smem_d[bEx + e - 1]);
-                    if (zy) b.Eb[1][o - 1] = z0pec ? 0.0 : eya + kk * (w1 - smem_d[bEy + e - 1]);
-                }
-                if (zw1 && (x.fl & kKNm1)) {
-                    const double kk = s_murz[ids[e + 1 + iofs]];
-                    if (zx) b.Eb[0][o + 1] = z1pec ? 0.0 : exa + kk * (w0 - smem_d[bEx + e + 1]);
-                    if (zy) b.Eb[1][o + 1] = z1pec ? 0.0 : eya + kk * (w1 - smem_d[bEy + e + 1]);
-                }
-                if (x.fl & kVX) b.Hb[0][o] = hx;
-                if (cellplane && (x.fl & kVKZ)) b.Hb[1][o] = hy;
-                if (cellplane && (x.fl & kVJY)) b.Hb[2][o] = hz;
+                hy_prev[v] = hy;
+                hz_prev[v] = hz;
             }
-            hy_prev[v] = hy;
-            hz_prev[v] = hz;
         }
     }
     __syncthreads();
     if (s_anymag) {
-        for (int r = 1 + tid; r <= g.max_iters; r += NT) {
+        for (int r = 1 + tid; r <= g.max_iters; r += blockDim.x) {
             const unsigned long long v = s_hist[r];
             if (v) atomicMax(&st->hist[r], v);
         }
