@@ -56,39 +56,40 @@ def _bytes_per_cell(f_mag: float) -> float:
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks + throttle reasons, timestamped; summary() keeps the
+    samples that fall inside [t0, t1] (the timed region)."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    Q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
         self.index = index
         self.proc = None
+        self.out = ""
 
-    def __enter__(self):
+    def start(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
+        time.sleep(0.3)
         return self
 
-    def __exit__(self, *exc):
+    def stop(self):
         if self.proc:
             self.proc.terminate()
             try:
                 self.out, _ = self.proc.communicate(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
-                self.out = ""
 
-    def summary(self):
-        if not self.proc or not getattr(self, "out", ""):
-            return None
-        sms, smax, reasons = [], 0, set()
+    def summary(self, t0: float, t1: float):
+        import datetime
+        rows = []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
                  "sw_power_cap"]
         for line in self.out.strip().splitlines():
@@ -96,17 +97,22 @@ class ClockSampler:
             if len(f) < 9:
                 continue
             try:
-                sms.append(float(f[1]))
-                smax = max(smax, float(f[2]))
+                ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                rows.append((ts, float(f[1]), float(f[2]), float(f[3]),
+                             [n for n, v in zip(names, f[5:9]) if v.lower() == "active"]))
             except ValueError:
                 continue
-            for n, v in zip(names, f[5:9]):
-                if v.lower() == "active":
-                    reasons.add(n)
-        if not sms:
+        if not rows:
             return None
-        return {"sm_mhz": statistics.median(sms), "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sms)}
+        inside = [r for r in rows if t0 - 0.05 <= r[0] <= t1 + 0.05]
+        if not inside:   # short region: the sample closest to its middle
+            mid = 0.5 * (t0 + t1)
+            inside = [min(rows, key=lambda r: abs(r[0] - mid))]
+        reasons = sorted({n for r in inside for n in r[4]})
+        return {"sm_mhz": statistics.median(r[1] for r in inside),
+                "sm_max_mhz": max(r[2] for r in rows),
+                "power_w_max": max(r[3] for r in inside),
+                "reasons": reasons, "samples": len(inside)}
 
 
 def synthetic_state(cfg, kind: str):
@@ -184,7 +190,7 @@ def run_reference(args) -> None:
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
@@ -241,17 +247,20 @@ def main() -> None:
     # timed region: K steps, device-resident state; dominant kernel timed by
     # CUDA events on its own stream (library stream) inside the same region
     dev.set_kernel_timing(True)
+    clk = ClockSampler(local).start()
     barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        dev.run_device(args.warmup, args.steps, src[args.warmup:].data_ptr(),
-                       probe[args.warmup:].data_ptr(), iters[args.warmup:].data_ptr(),
-                       stream.cuda_stream)
-        e1.record(stream)
-        torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    t_wall0 = time.time()
+    e0.record(stream)
+    dev.run_device(args.warmup, args.steps, src[args.warmup:].data_ptr(),
+                   probe[args.warmup:].data_ptr(), iters[args.warmup:].data_ptr(),
+                   stream.cuda_stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t_wall1 = time.time()
+    clk.stop()
     barrier()
     ms = e0.elapsed_time(e1)
     launches = dev.launch_count()
@@ -320,7 +329,7 @@ def main() -> None:
                      "kernel_ms_per_step": per_launch_ms,
                      "kernel_share_of_step": per_launch_ms / (ms / args.steps)},
         "cpu_baseline": cpu,
-        "clocks": clk.summary(),
+        "clocks": clk.summary(t_wall0, t_wall1),
         "gpu_launches": launches,
     }
     print(json.dumps(line))

@@ -45,6 +45,10 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
     // entries per CTA per plane: 2 per thread unless the plane is small
     fs->V = g.FyFz >= 8 * kSweepThreads * sms ? 4 : (g.FyFz >= 2 * kSweepThreads * 64 ? 2 : 1);
     sc.T = fs->V * kSweepThreads;
+    if (const char* e = getenv("MPB_SWEEP_T")) {
+        const int t = atoi(e);
+        if (t > 0 && t <= sc.T) sc.T = t;
+    }
     sc.tiles = (g.FyFz + sc.T - 1) / sc.T;
     {
         bool fastdiv = true;
@@ -58,14 +62,16 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
     sc.stage_bytes = ((3 * sc.ecap + 3 * sc.hcap) * 8 + sc.icap + 127) / 128 * 128;
     sc.ring_offset = ((g.max_iters + 2) * 8 + 127) / 128 * 128;
     fs->smem = (size_t)sc.ring_offset + (size_t)kSlots * sc.stage_bytes;
-    if (const char* e = getenv("MPB_SWEEP_WAVES")) (void)e;
+
     const size_t static_smem = 8 * 1024;
     if (fs->smem + static_smem > (size_t)smem_optin)
         return fail_msg(MPB_EINVAL, "fused sweep staging (%zu B) exceeds shared memory",
                         fs->smem);
     // x-chunks: ~8 waves of one CTA per SM, chunks of >= 24 planes
     const int Fx = g.F[0];
-    const int want = std::max(1, (8 * sms + sc.tiles - 1) / sc.tiles);
+    int waves = 16;
+    if (const char* e = getenv("MPB_SWEEP_WAVES")) waves = std::max(1, atoi(e));
+    const int want = std::max(1, (waves * sms + sc.tiles - 1) / sc.tiles);
     const int maxch = std::max(1, Fx / 24);
     sc.nchunks = std::max(1, std::min(want, maxch));
     sc.chunk = (Fx + sc.nchunks - 1) / sc.nchunks;
