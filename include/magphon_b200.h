@@ -91,6 +91,19 @@ typedef struct mpb_setup {
     int32_t device;         /* CUDA ordinal                                   */
     int32_t kernel_variant; /* 0 = default (fused sweep), 1 = split H/E sweeps */
     int32_t graph_steps;    /* steps per captured CUDA graph (0 = default)    */
+    /* x-slab decomposition.  Single GPU: nranks = 1, x_lo = 0,
+     * x_hi = n[0].  This rank owns cell planes [x_lo, x_hi) (the last rank
+     * also the field plane n[0]); cell_material then covers cell planes
+     * [max(0, x_lo-1), min(n[0], x_hi+1)) and the state arrays of
+     * mpb_load_state / mpb_save_state cover field planes
+     * [max(0, x_lo-1), min(F[0], x_hi'+1)) with x_hi' = F[0] on the last
+     * rank (one ghost plane per side).  Boundary planes travel over NCCL at
+     * the end of every step; the LLG residual history is all-reduced. */
+    int32_t nranks;
+    int32_t rank;
+    int32_t x_lo, x_hi;
+    int32_t any_magnetic;   /* 1 if any rank owns magnetic cells             */
+    uint8_t nccl_id[128];   /* ncclUniqueId from mpb_nccl_unique_id (rank 0) */
 } mpb_setup;
 
 /* Failure record of an LLG step (llg.py:139-148 + sim.py:161-164). */
@@ -98,13 +111,19 @@ typedef struct mpb_failure {
     int64_t step;           /* -1 if no failure                                */
     double residual;
     int32_t iterations;
-    int32_t kind;           /* 1 = diverging, 2 = budget exhausted            */
+    int32_t kind;           /* 1 = diverging, 2 = budget exhausted,
+                               3 = multi-rank: global residual non-monotone at r*
+                                   (unsupported across ranks; reported, not guessed) */
 } mpb_failure;
 
 typedef struct mpb_handle mpb_handle;
 
 /* Library / build identification, e.g. "magphon_b200 0.1 sm_100a fmad=false". */
 MPB_API const char* mpb_version(void);
+
+/* NCCL unique id for a multi-rank run (call on rank 0, broadcast the 128
+ * bytes to every rank, pass in mpb_setup.nccl_id). */
+MPB_API int mpb_nccl_unique_id(uint8_t out[128]);
 
 /* Message of the last error on this thread ("" if none). */
 MPB_API const char* mpb_last_error(void);
@@ -144,6 +163,17 @@ MPB_API int mpb_run(mpb_handle* h, int64_t n0, int64_t nsteps, const double* src
 MPB_API int mpb_run_device(mpb_handle* h, int64_t n0, int64_t nsteps,
                    const double* d_src_vals, double* d_probe_out,
                    int32_t* d_iters_out, void* stream);
+
+/* In-process emulation of an n-rank slab decomposition on ONE device (test
+ * and validation entry point; production runs use one process per GPU and
+ * NCCL).  hs[r] is rank r, created with nranks = n and an all-zero nccl_id.
+ * The ranks are stepped in lockstep on one stream with exactly the kernels of
+ * the NCCL path; the boundary planes move by device copies and the LLG
+ * all-reduce is a kernel.  probe_out[r] receives rank r's probe rows (zeros
+ * for probes it does not own); iters_out receives r* per step. */
+MPB_API int mpb_group_run(mpb_handle* const* hs, int32_t n, int64_t n0, int64_t nsteps,
+                          const double* src_vals, double* const* probe_out,
+                          int32_t* iters_out, mpb_failure* fail);
 
 /* Synchronise and report the first LLG failure since the last call. */
 MPB_API int mpb_check_failure(mpb_handle* h, mpb_failure* fail);

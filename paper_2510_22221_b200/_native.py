@@ -42,7 +42,10 @@ class Setup(C.Structure):
                 ("probe_loc", C.POINTER(C.c_int32)),
                 ("llg_tol", C.c_double), ("llg_max_iters", C.c_int32),
                 ("device", C.c_int32), ("kernel_variant", C.c_int32),
-                ("graph_steps", C.c_int32)]
+                ("graph_steps", C.c_int32),
+                ("nranks", C.c_int32), ("rank", C.c_int32),
+                ("x_lo", C.c_int32), ("x_hi", C.c_int32),
+                ("any_magnetic", C.c_int32), ("nccl_id", C.c_uint8 * 128)]
 
 
 class Failure(C.Structure):
@@ -50,10 +53,11 @@ class Failure(C.Structure):
                 ("iterations", C.c_int32), ("kind", C.c_int32)]
 
 
-EXPORTS = ("mpb_version", "mpb_last_error", "mpb_create", "mpb_destroy",
+EXPORTS = ("mpb_version", "mpb_last_error", "mpb_nccl_unique_id", "mpb_create", "mpb_destroy",
            "mpb_load_state", "mpb_save_state", "mpb_run", "mpb_run_device",
            "mpb_check_failure", "mpb_set_kernel_timing", "mpb_kernel_time",
-           "mpb_launch_count", "mpb_device_bytes", "mpb_selftest_division")
+           "mpb_launch_count", "mpb_device_bytes", "mpb_selftest_division",
+           "mpb_group_run")
 
 _lib = None
 
@@ -75,6 +79,7 @@ def load_library(path: os.PathLike | None = None) -> C.CDLL:
     proto = {
         "mpb_version": (C.c_char_p, []),
         "mpb_last_error": (C.c_char_p, []),
+        "mpb_nccl_unique_id": (C.c_int, [P(C.c_uint8)]),
         "mpb_create": (C.c_int, [P(Setup), P(C.c_void_p)]),
         "mpb_destroy": (None, [C.c_void_p]),
         "mpb_load_state": (C.c_int, [C.c_void_p, dbl_pp, P(C.c_double)]),
@@ -92,6 +97,9 @@ def load_library(path: os.PathLike | None = None) -> C.CDLL:
         "mpb_device_bytes": (C.c_int64, [C.c_void_p]),
         "mpb_selftest_division": (C.c_int, [C.c_int32, C.c_double, P(C.c_double),
                                             C.c_int64, P(C.c_int64), P(C.c_double)]),
+        "mpb_group_run": (C.c_int, [P(C.c_void_p), C.c_int32, C.c_int64, C.c_int64,
+                                    P(C.c_double), P(P(C.c_double)), P(C.c_int32),
+                                    P(Failure)]),
     }
     for name, (res, args) in proto.items():
         fn = getattr(lib, name)

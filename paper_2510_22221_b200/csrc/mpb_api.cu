@@ -1,8 +1,10 @@
 // mpb_api.cu -- C ABI of the B200 Maxwell-LLG stepper (include/magphon_b200.h).
 //
-// Owns device memory, streams and CUDA graphs for one run; sequences the
-// per-step kernels.  Build: see paper_2510_22221_b200/csrc/Makefile.
+// Owns device memory, streams, CUDA graphs and (multi-rank) the NCCL
+// communicator of one run; sequences the per-step kernels.
+// Build: paper_2510_22221_b200/csrc/Makefile.
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -42,6 +44,14 @@ int fail_msg(int code, const char* fmt, ...) {
                             cudaGetErrorString(e_), __FILE__, __LINE__);          \
     } while (0)
 
+#define NC(call)                                                                  \
+    do {                                                                          \
+        ncclResult_t r_ = (call);                                                 \
+        if (r_ != ncclSuccess)                                                    \
+            return fail_msg(MPB_ECUDA, "%s failed: %s (%s:%d)", #call,            \
+                            ncclGetErrorString(r_), __FILE__, __LINE__);          \
+    } while (0)
+
 constexpr int kDefaultGraphSteps = 16;
 constexpr int64_t kRunChunk = 1 << 16;   // steps per host<->device staging chunk
 
@@ -52,16 +62,24 @@ struct mpb_handle {
     Geom g{};
     int variant = 0;
     int graph_steps = kDefaultGraphSteps;
-    int Fx = 1;
-    int64_t nentries = 0;          // Fx * PP
+    // slab: local field planes [lo, hi); owned [g.c0, g.c1); cell planes
+    // [clo, chi) of the host material / M arrays
+    int nranks = 1, rank = 0;
+    int lo = 0, hi = 1, clo = 0, chi = 1;
+    int any_magnetic = 0;
+    ncclComm_t comm = nullptr;
+    int64_t nloc = 0;              // (hi - lo) * PP
     int64_t mplanes = 0;           // mx1 - mx0
-    double* E[2][3] = {};
+    double* E[2][3] = {};          // allocations (local planes)
     double* H[2][3] = {};
     double* M[2][3] = {};
-    uint8_t* ids = nullptr;
+    uint8_t* ids = nullptr;        // allocation (local planes)
     mpb_material* mats = nullptr;
-    int2* magcells = nullptr;
-    int nmag = 0;
+    int nmat_table = 0;
+    int2* magcells = nullptr;      // local magnetic cells (owned + ghost plane)
+    unsigned char* magowned = nullptr;
+    int nmag = 0;                  // local cells (incl. ghost copies)
+    int nmag_owned = 0;
     double* scratch = nullptr;
     StepState* st = nullptr;
     ProbeDesc* probes = nullptr;
@@ -79,7 +97,8 @@ struct mpb_handle {
     int64_t stage_cap = 0;
     cudaStream_t stream = nullptr;
     cudaGraphExec_t graph[2] = {nullptr, nullptr};
-    // host copy of M (cells outside the device M range never change)
+    // host copy of M on the local cell planes (cells outside the device M
+    // range never change)
     std::vector<double> hostM;
     // timing
     int timing = 0;
@@ -88,13 +107,11 @@ struct mpb_handle {
     int64_t timed_launches = 0;
     int64_t launches_last = 0;
     int64_t bytes = 0;
-    int nmat_table = 0;
     void* fused = nullptr;         // FusedState (mpb_fused.cuh)
 };
 
-
 namespace {
-// Fused single-sweep variant hooks (filled in by mpb_fused.cuh).
+// Fused single-sweep variant hooks (mpb_fused.cuh).
 int prepare_fused(mpb_handle* h, const Geom& g);
 void destroy_fused(mpb_handle* h);
 int launch_fused(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s);
@@ -106,19 +123,28 @@ const char* fused_kernel_name();
 
 namespace {
 
+// View pointers: buffers are addressed with GLOBAL plane indices in every
+// kernel; the allocation holds planes [lo, hi), so the view is offset.
+template <typename T>
+T* view(T* alloc, const mpb_handle* h) {
+    return alloc ? alloc - (int64_t)h->lo * h->g.PP : nullptr;
+}
+
 Bufs make_bufs(const mpb_handle* h, int pa) {
     Bufs b{};
     const int pb = 1 - pa;
     for (int c = 0; c < 3; ++c) {
-        b.Ea[c] = h->E[pa][c];
-        b.Ha[c] = h->H[pa][c];
-        b.Ma[c] = h->M[pa][c];
-        b.Eb[c] = h->E[pb][c];
-        b.Hb[c] = h->H[pb][c];
+        b.Ea[c] = view(h->E[pa][c], h);
+        b.Ha[c] = view(h->H[pa][c], h);
+        b.Ma[c] = h->M[pa][c];      // M arrays are indexed (i - mx0) already
+        b.Eb[c] = view(h->E[pb][c], h);
+        b.Hb[c] = view(h->H[pb][c], h);
         b.Mb[c] = h->M[pb][c];
     }
     return b;
 }
+
+const uint8_t* ids_view(const mpb_handle* h) { return view(h->ids, h); }
 
 template <typename T>
 int dev_alloc(mpb_handle* h, T** p, size_t count) {
@@ -132,84 +158,125 @@ int dev_alloc(mpb_handle* h, T** p, size_t count) {
 int reset_state(mpb_handle* h) {
     StepState s{};
     memset(&s, 0, sizeof s);
-    s.rc_min = 0x7fffffff;
+    s.rc_negmin = -0x7fffffff;
     s.fail_step = -1;
     CU(cudaMemcpyAsync(h->st, &s, sizeof s, cudaMemcpyHostToDevice, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
     return MPB_OK;
 }
 
-// Enqueue one coupled step reading buffer set `pa`.
-int enqueue_step(mpb_handle* h, int pa, bool timed) {
+// End-of-step boundary exchange over NCCL (multi-rank): the last owned plane
+// (E, H and M when magnetic) goes up to rank+1's low ghost plane, the first
+// owned plane (E) goes down to rank-1's high ghost plane.  Operates on the
+// buffer set `pb` that holds the state after the step.
+int exchange(mpb_handle* h, int pb, cudaStream_t s) {
+    const Geom& g = h->g;
+    const size_t n = (size_t)g.PP;
+    auto plane = [&](double* alloc, int i) { return alloc + (int64_t)(i - h->lo) * g.PP; };
+    auto mplane = [&](double* alloc, int i) { return alloc + (int64_t)(i - g.mx0) * g.PP; };
+    auto has_m = [&](int i) { return h->mplanes > 0 && i >= g.mx0 && i < g.mx1; };
+    NC(ncclGroupStart());
+    if (h->rank + 1 < h->nranks) {
+        const int up = h->rank + 1;
+        for (int c = 0; c < 3; ++c) {
+            NC(ncclSend(plane(h->E[pb][c], g.c1 - 1), n, ncclDouble, up, h->comm, s));
+            NC(ncclSend(plane(h->H[pb][c], g.c1 - 1), n, ncclDouble, up, h->comm, s));
+            if (has_m(g.c1 - 1))
+                NC(ncclSend(mplane(h->M[pb][c], g.c1 - 1), n, ncclDouble, up, h->comm, s));
+            NC(ncclRecv(plane(h->E[pb][c], g.c1), n, ncclDouble, up, h->comm, s));
+        }
+    }
+    if (h->rank > 0) {
+        const int dn = h->rank - 1;
+        for (int c = 0; c < 3; ++c) {
+            NC(ncclRecv(plane(h->E[pb][c], g.c0 - 1), n, ncclDouble, dn, h->comm, s));
+            NC(ncclRecv(plane(h->H[pb][c], g.c0 - 1), n, ncclDouble, dn, h->comm, s));
+            if (has_m(g.c0 - 1))
+                NC(ncclRecv(mplane(h->M[pb][c], g.c0 - 1), n, ncclDouble, dn, h->comm, s));
+            NC(ncclSend(plane(h->E[pb][c], g.c0), n, ncclDouble, dn, h->comm, s));
+        }
+    }
+    NC(ncclGroupEnd());
+    return MPB_OK;
+}
+
+// ---- step phases (shared by the NCCL path and the in-process group) ----
+
+int phase_sweep(mpb_handle* h, int pa, cudaStream_t s, int64_t& launches) {
     const Geom& g = h->g;
     const Bufs b = make_bufs(h, pa);
-    cudaStream_t s = h->stream;
-    int64_t launches = 0;
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (timed) {
-        CU(cudaEventCreate(&e0));
-        CU(cudaEventCreate(&e1));
-        CU(cudaEventRecord(e0, s));
-    }
     const size_t hist_smem = (size_t)(g.max_iters + 2) * sizeof(unsigned long long);
+    const dim3 plane_grid((g.FyFz + 255) / 256, g.c1 - g.c0);
     if (h->variant == 1) {
-        dim3 grid((g.FyFz + 255) / 256, h->Fx);
-        k_hsweep<<<grid, 256, hist_smem, s>>>(g, b, h->mats, h->ids, h->st);
-        ++launches;
+        k_hsweep<<<plane_grid, 256, hist_smem, s>>>(g, b, h->mats, ids_view(h), h->st);
     } else {
         int rc = launch_fused(h, g, b, s);
         if (rc) return rc;
+    }
+    ++launches;
+    return MPB_OK;
+}
+
+int phase_fixup_single(mpb_handle* h, int pa, cudaStream_t s, int64_t& launches) {
+    if (h->nmag == 0) return MPB_OK;
+    const Geom& g = h->g;
+    const Bufs b = make_bufs(h, pa);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(h->fixup_blocks);
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    MagScratch scr{h->scratch};
+    CU(cudaLaunchKernelEx(&cfg, k_llg_fixup, g, b, (const mpb_material*)h->mats, ids_view(h),
+                          (const int2*)h->magcells, h->nmag, scr, h->st));
+    ++launches;
+    return MPB_OK;
+}
+
+int phase_topup(mpb_handle* h, int pa, cudaStream_t s, int64_t& launches) {
+    if (h->nmag == 0) return MPB_OK;
+    const Bufs b = make_bufs(h, pa);
+    k_llg_topup<<<(h->nmag + 255) / 256, 256, 0, s>>>(h->g, b, h->mats, ids_view(h),
+                                                      h->magcells, h->magowned, h->nmag,
+                                                      h->st);
+    ++launches;
+    return MPB_OK;
+}
+
+int phase_decide(mpb_handle* h, cudaStream_t s, int64_t& launches) {
+    k_llg_decide<<<1, 32, 0, s>>>(h->g, h->st);
+    ++launches;
+    return MPB_OK;
+}
+
+// after r* is settled: deferred E, x/y walls, z-wall fix-up, source + probes
+int phase_post(mpb_handle* h, int pa, cudaStream_t s, int64_t& launches,
+               bool esweep = true) {
+    const Geom& g = h->g;
+    const Bufs b = make_bufs(h, pa);
+    const uint8_t* ids = ids_view(h);
+    if (h->variant != 1 && h->nmag > 0) {
+        int rc = launch_deferred(h, g, b, s);
+        if (rc) return rc;
         ++launches;
     }
-    if (timed && h->variant == 1) CU(cudaEventRecord(e1, s));
-    if (h->nmag > 0) {
-        cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3(h->fixup_blocks);
-        cfg.blockDim = dim3(256);
-        cfg.stream = s;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeCooperative;
-        attr[0].val.cooperative = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        MagScratch scr{h->scratch};
-        CU(cudaLaunchKernelEx(&cfg, k_llg_fixup, g, b, (const mpb_material*)h->mats,
-                              (const uint8_t*)h->ids, (const int2*)h->magcells, h->nmag,
-                              scr, h->st));
+    if (h->variant == 1 && esweep) {
+        const dim3 plane_grid((g.FyFz + 255) / 256, g.c1 - g.c0);
+        k_esweep<<<plane_grid, 256, 0, s>>>(g, b, h->mats, ids, h->st);
         ++launches;
-        if (h->variant != 1) {
-            // fused sweep: E entries next to magnetic cells are recomputed
-            // once r* is settled
-            int rc = launch_deferred(h, g, b, s);
-            if (rc) return rc;
-            ++launches;
-        }
     }
-    if (h->variant == 1) {
-        cudaEvent_t ea = nullptr, eb = nullptr;
-        if (timed) {
-            CU(cudaEventCreate(&ea));
-            CU(cudaEventCreate(&eb));
-            CU(cudaEventRecord(ea, s));
-        }
-        dim3 grid((g.FyFz + 255) / 256, h->Fx);
-        k_esweep<<<grid, 256, 0, s>>>(g, b, h->mats, h->ids, h->st);
-        ++launches;
-        if (timed) {
-            CU(cudaEventRecord(eb, s));
-            h->events.emplace_back(ea, eb);
-        }
-    }
-    if (timed && h->variant != 1) CU(cudaEventRecord(e1, s));
-    if (timed) h->events.emplace_back(e0, e1);
-    // fused variant: z walls are applied inside the sweep (+ k_zfix below)
-    const int nface = h->variant == 1 ? 6 : 4;
+    const int nface = h->variant == 1 ? 6 : 4;   // fused: z walls are in the sweep
     for (int face = 0; face < nface; ++face) {
         if (!h->faces_active[face]) continue;
         const int axis = face >> 1;
         const int u = axis == 0 ? 1 : 0, w = axis == 2 ? 1 : 2;
-        const int64_t cnt = (int64_t)g.F[u] * g.F[w];
-        k_wall<<<(unsigned)((cnt + 255) / 256), 256, 0, s>>>(g, b, h->mats, h->ids, h->st,
-                                                            face);
+        const int64_t nu = u == 0 ? g.c1 - g.c0 : g.F[u];
+        const int64_t cnt = nu * g.F[w];
+        k_wall<<<(unsigned)((cnt + 255) / 256), 256, 0, s>>>(g, b, h->mats, ids, h->st, face);
         ++launches;
     }
     if (h->variant != 1) {
@@ -218,9 +285,114 @@ int enqueue_step(mpb_handle* h, int pa, bool timed) {
         launches += zfix_launches(h);
     }
     k_finish<<<1, 256, 0, s>>>(g, b, h->src, h->probes, h->nprobes, 1 - pa,
-                               h->nmag > 0 ? 1 : 0, h->st);
+                               h->any_magnetic ? 1 : 0, h->st);
     ++launches;
+    return MPB_OK;
+}
+
+// Enqueue one coupled step reading buffer set `pa` (single rank or NCCL).
+int enqueue_step(mpb_handle* h, int pa, bool timed) {
+    const Geom& g = h->g;
+    cudaStream_t s = h->stream;
+    int64_t launches = 0;
+    int rc;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (timed) {
+        CU(cudaEventCreate(&e0));
+        CU(cudaEventCreate(&e1));
+        CU(cudaEventRecord(e0, s));
+    }
+    if ((rc = phase_sweep(h, pa, s, launches))) return rc;
+    if (timed) {
+        CU(cudaEventRecord(e1, s));
+        h->events.emplace_back(e0, e1);
+    }
+    if (h->nranks == 1) {
+        if ((rc = phase_fixup_single(h, pa, s, launches))) return rc;
+    } else if (h->any_magnetic) {
+        // global r*: all-reduce the residual history and local-stop range
+        NC(ncclGroupStart());
+        NC(ncclAllReduce(&h->st->hist[1], &h->st->hist[1], (size_t)g.max_iters, ncclUint64,
+                         ncclMax, h->comm, s));
+        NC(ncclAllReduce(&h->st->rc_max, &h->st->rc_max, 2, ncclInt32, ncclMax, h->comm, s));
+        NC(ncclGroupEnd());
+        if ((rc = phase_topup(h, pa, s, launches))) return rc;
+        NC(ncclAllReduce(&h->st->hist2[1], &h->st->hist2[1], (size_t)g.max_iters, ncclUint64,
+                         ncclMax, h->comm, s));
+        if ((rc = phase_decide(h, s, launches))) return rc;
+    }
+    if (timed && h->variant == 1) {   // split variant: time the E sweep too
+        cudaEvent_t ea = nullptr, eb = nullptr;
+        CU(cudaEventCreate(&ea));
+        CU(cudaEventCreate(&eb));
+        CU(cudaEventRecord(ea, s));
+        const Bufs b = make_bufs(h, pa);
+        const dim3 plane_grid((g.FyFz + 255) / 256, g.c1 - g.c0);
+        k_esweep<<<plane_grid, 256, 0, s>>>(g, b, h->mats, ids_view(h), h->st);
+        CU(cudaEventRecord(eb, s));
+        h->events.emplace_back(ea, eb);
+        ++launches;
+        if ((rc = phase_post(h, pa, s, launches, false))) return rc;
+    } else {
+        if ((rc = phase_post(h, pa, s, launches))) return rc;
+    }
+    if (h->nranks > 1) {
+        if ((rc = exchange(h, 1 - pa, s))) return rc;
+    }
     h->launches_last += launches;
+    CU(cudaGetLastError());
+    return MPB_OK;
+}
+
+// In-process group: the boundary exchange of exchange() as device copies.
+int exchange_group(mpb_handle* const* hs, int n, int pb, cudaStream_t s) {
+    for (int r = 0; r + 1 < n; ++r) {
+        mpb_handle* a = hs[r];
+        mpb_handle* b = hs[r + 1];
+        const Geom& ga = a->g;
+        const Geom& gb = b->g;
+        const size_t bytes = (size_t)ga.PP * sizeof(double);
+        auto plane = [](mpb_handle* h, double* alloc, int i) {
+            return alloc + (int64_t)(i - h->lo) * h->g.PP;
+        };
+        const int up_src = ga.c1 - 1;   // a's last owned plane -> b's low ghost
+        const int dn_src = gb.c0;       // b's first owned plane -> a's high ghost
+        const bool m_up = a->mplanes > 0 && up_src >= ga.mx0 && up_src < ga.mx1;
+        for (int c = 0; c < 3; ++c) {
+            CU(cudaMemcpyAsync(plane(b, b->E[pb][c], up_src), plane(a, a->E[pb][c], up_src),
+                               bytes, cudaMemcpyDeviceToDevice, s));
+            CU(cudaMemcpyAsync(plane(b, b->H[pb][c], up_src), plane(a, a->H[pb][c], up_src),
+                               bytes, cudaMemcpyDeviceToDevice, s));
+            if (m_up)
+                CU(cudaMemcpyAsync(b->M[pb][c] + (int64_t)(up_src - gb.mx0) * gb.PP,
+                                   a->M[pb][c] + (int64_t)(up_src - ga.mx0) * ga.PP, bytes,
+                                   cudaMemcpyDeviceToDevice, s));
+            CU(cudaMemcpyAsync(plane(a, a->E[pb][c], dn_src), plane(b, b->E[pb][c], dn_src),
+                               bytes, cudaMemcpyDeviceToDevice, s));
+        }
+    }
+    return MPB_OK;
+}
+
+int group_step(mpb_handle* const* hs, int n, int pa, cudaStream_t s) {
+    int rc;
+    int64_t launches = 0;
+    for (int r = 0; r < n; ++r)
+        if ((rc = phase_sweep(hs[r], pa, s, launches))) return rc;
+    if (hs[0]->any_magnetic) {
+        StatePtrs sp{};
+        sp.n = n;
+        for (int r = 0; r < n; ++r) sp.s[r] = hs[r]->st;
+        k_group_reduce<<<1, 256, 0, s>>>(sp, hs[0]->g.max_iters, 0);
+        for (int r = 0; r < n; ++r)
+            if ((rc = phase_topup(hs[r], pa, s, launches))) return rc;
+        k_group_reduce<<<1, 256, 0, s>>>(sp, hs[0]->g.max_iters, 1);
+        for (int r = 0; r < n; ++r)
+            if ((rc = phase_decide(hs[r], s, launches))) return rc;
+    }
+    for (int r = 0; r < n; ++r)
+        if ((rc = phase_post(hs[r], pa, s, launches))) return rc;
+    if ((rc = exchange_group(hs, n, 1 - pa, s))) return rc;
     CU(cudaGetLastError());
     return MPB_OK;
 }
@@ -242,11 +414,13 @@ int build_graph(mpb_handle* h, int start_parity) {
     return MPB_OK;
 }
 
-int64_t launches_per_step(const mpb_handle* h) {
+int64_t launches_per_step(mpb_handle* h) {
     int64_t n = (h->variant == 1 ? 2 : 1) + 1;
-    if (h->nmag > 0) n += (h->variant == 1 ? 1 : 2);
+    if (h->nranks == 1 && h->nmag > 0) n += 1;
+    if (h->nranks > 1 && h->any_magnetic) n += 1 + (h->nmag > 0 ? 1 : 0);
+    if (h->variant != 1 && h->nmag > 0) n += 1;
     for (int f = 0; f < (h->variant == 1 ? 6 : 4); ++f) n += h->faces_active[f];
-    if (h->variant != 1) n += zfix_launches(const_cast<mpb_handle*>(h));
+    if (h->variant != 1) n += zfix_launches(h);
     return n;
 }
 
@@ -276,24 +450,17 @@ int enqueue_steps(mpb_handle* h, int64_t nsteps) {
 
 int set_run_buffers(mpb_handle* h, int64_t n0, const double* src, double* probe,
                     int* iters) {
-    struct {
-        long long step, local;
-        const double* s;
-        double* p;
-        int* it;
-    } v{n0, 0, src, probe, iters};
-    // step, local, src_vals, probe_out, iters_out are laid out contiguously
-    static_assert(offsetof(StepState, local) == offsetof(StepState, step) + 8, "layout");
-    CU(cudaMemcpyAsync(&h->st->step, &v.step, sizeof(long long), cudaMemcpyHostToDevice,
+    const long long step = n0, local = 0;
+    CU(cudaMemcpyAsync(&h->st->step, &step, sizeof step, cudaMemcpyHostToDevice, h->stream));
+    CU(cudaMemcpyAsync(&h->st->local, &local, sizeof local, cudaMemcpyHostToDevice,
                        h->stream));
-    CU(cudaMemcpyAsync(&h->st->local, &v.local, sizeof(long long),
-                       cudaMemcpyHostToDevice, h->stream));
-    CU(cudaMemcpyAsync(&h->st->src_vals, &v.s, sizeof(void*), cudaMemcpyHostToDevice,
+    CU(cudaMemcpyAsync(&h->st->src_vals, &src, sizeof(void*), cudaMemcpyHostToDevice,
                        h->stream));
-    CU(cudaMemcpyAsync(&h->st->probe_out, &v.p, sizeof(void*), cudaMemcpyHostToDevice,
+    CU(cudaMemcpyAsync(&h->st->probe_out, &probe, sizeof(void*), cudaMemcpyHostToDevice,
                        h->stream));
-    CU(cudaMemcpyAsync(&h->st->iters_out, &v.it, sizeof(void*), cudaMemcpyHostToDevice,
+    CU(cudaMemcpyAsync(&h->st->iters_out, &iters, sizeof(void*), cudaMemcpyHostToDevice,
                        h->stream));
+    CU(cudaStreamSynchronize(h->stream));   // host locals above must outlive the copies
     return MPB_OK;
 }
 
@@ -310,6 +477,41 @@ int read_failure(mpb_handle* h, mpb_failure* fail) {
     return s.fail ? MPB_ESTEP : MPB_OK;
 }
 
+int upload_probes(mpb_handle* h) {
+    const Geom& g = h->g;
+    std::vector<ProbeDesc> pd((size_t)std::max(1, h->nprobes));
+    const int ny = g.n[1], nz = g.n[2];
+    const int ncl = h->chi - h->clo;
+    for (int p = 0; p < h->nprobes; ++p) {
+        const int comp = h->probe_comp[p];
+        const int* L = &h->probe_loc[3 * p];
+        const int64_t f = (int64_t)L[1] * g.F[2] + L[2];
+        ProbeDesc d{};
+        const bool owned = L[0] >= g.c0 && L[0] < g.c1;   // other ranks report 0
+        if (!owned) {
+            d.ptr0 = d.ptr1 = nullptr;
+            d.constant = 0.0;
+        } else if (comp < MPB_COMP_HX) {
+            d.ptr0 = view(h->E[0][comp], h); d.ptr1 = view(h->E[1][comp], h);
+            d.off = L[0] * g.PP + f;
+        } else if (comp < MPB_COMP_MX) {
+            d.ptr0 = view(h->H[0][comp - 3], h); d.ptr1 = view(h->H[1][comp - 3], h);
+            d.off = L[0] * g.PP + f;
+        } else if (L[0] >= g.mx0 && L[0] < g.mx1) {
+            d.ptr0 = h->M[0][comp - 6]; d.ptr1 = h->M[1][comp - 6];
+            d.off = (int64_t)(L[0] - g.mx0) * g.PP + f;
+        } else {
+            d.ptr0 = d.ptr1 = nullptr;
+            d.constant =
+                h->hostM[(((size_t)(comp - 6) * ncl + (L[0] - h->clo)) * ny + L[1]) * nz + L[2]];
+        }
+        pd[(size_t)p] = d;
+    }
+    CU(cudaMemcpy(h->probes, pd.data(), sizeof(ProbeDesc) * pd.size(),
+                  cudaMemcpyHostToDevice));
+    return MPB_OK;
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -318,10 +520,20 @@ int read_failure(mpb_handle* h, mpb_failure* fail) {
 extern "C" {
 
 const char* mpb_version(void) {
-    return "magphon_b200 0.1 sm_100a fp64 fmad=false";
+    return "magphon_b200 0.2 sm_100a fp64 fmad=false nccl";
 }
 
 const char* mpb_last_error(void) { return g_err.c_str(); }
+
+int mpb_nccl_unique_id(uint8_t out[128]) {
+    g_err.clear();
+    if (!out) return fail_msg(MPB_EINVAL, "null argument");
+    ncclUniqueId id;
+    NC(ncclGetUniqueId(&id));
+    static_assert(sizeof(id) == 128, "ncclUniqueId size");
+    memcpy(out, &id, 128);
+    return MPB_OK;
+}
 
 int mpb_create(const mpb_setup* su, mpb_handle** out) {
     g_err.clear();
@@ -344,10 +556,27 @@ int mpb_create(const mpb_setup* su, mpb_handle** out) {
         if (su->faces[f] == MPB_FACE_MUR1 && su->n[f >> 1] <= 1)
             return fail_msg(MPB_EINVAL, "MUR1 on collapsed axis face %d", f);
     }
+    const int nranks = std::max(1, su->nranks);
+    const int nx = su->n[0], ny = su->n[1], nz = su->n[2];
+    const int x_lo = nranks == 1 ? 0 : su->x_lo;
+    const int x_hi = nranks == 1 ? nx : su->x_hi;
+    if (nranks > 1) {
+        if (su->rank < 0 || su->rank >= nranks)
+            return fail_msg(MPB_EINVAL, "rank %d out of range", su->rank);
+        if (nx < 2 || x_lo < 0 || x_hi > nx || x_hi - x_lo < 2)
+            return fail_msg(MPB_EINVAL, "slab [%d,%d) of %d cells: need >= 2 planes per rank",
+                            x_lo, x_hi, nx);
+        if ((su->rank == 0) != (x_lo == 0) || (su->rank == nranks - 1) != (x_hi == nx))
+            return fail_msg(MPB_EINVAL, "slab ranges must be ordered by rank");
+        if (su->kernel_variant == 1)
+            return fail_msg(MPB_EINVAL, "multi-rank runs use the fused sweep (variant 0)");
+    }
     auto* h = new mpb_handle();
     h->device = su->device;
     h->variant = su->kernel_variant;
     h->graph_steps = su->graph_steps > 0 ? su->graph_steps : kDefaultGraphSteps;
+    h->nranks = nranks;
+    h->rank = nranks == 1 ? 0 : su->rank;
     CU(cudaSetDevice(h->device));
     CU(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
 
@@ -362,16 +591,28 @@ int mpb_create(const mpb_setup* su, mpb_handle** out) {
     }
     g.FyFz = (int)(F[1] * F[2]);
     g.PP = (F[1] * F[2] + 31) / 32 * 32;
-    g.coef_h = su->coef_h;
-    for (int f = 0; f < 6; ++f) {
-        g.faces[f] = su->faces[f];
-        h->faces_active[f] = g.act[f >> 1] && su->faces[f] != MPB_FACE_PMC;
+    if ((uint64_t)F[0] * (uint64_t)g.PP >= (1ull << 32)) {
+        mpb_destroy(h);
+        return fail_msg(MPB_EINVAL, "grid too large for 32-bit element offsets");
     }
+    g.coef_h = su->coef_h;
     g.max_iters = su->llg_max_iters;
     g.tol = su->llg_tol;
-    h->Fx = (int)F[0];
+    g.c0 = x_lo;
+    g.c1 = x_hi == nx ? (int)F[0] : x_hi;
+    h->lo = std::max(0, g.c0 - 1);
+    h->hi = std::min((int)F[0], g.c1 + 1);
+    h->clo = std::max(0, x_lo - 1);
+    h->chi = std::min(nx, x_hi + 1);
+    for (int f = 0; f < 6; ++f) {
+        g.faces[f] = su->faces[f];
+        bool act = g.act[f >> 1] && su->faces[f] != MPB_FACE_PMC;
+        if (f == 0 && g.c0 != 0) act = false;            // x walls on the end ranks
+        if (f == 1 && g.c1 != (int)F[0]) act = false;
+        h->faces_active[f] = act;
+    }
+    h->nloc = (int64_t)(h->hi - h->lo) * g.PP;
     h->nmat_table = MPB_MAX_MATERIALS;
-    h->nentries = F[0] * g.PP;
 
     // material table renumbered so that magnetic materials carry bit 7 of
     // the id (the sweep tests magnetism without a table lookup)
@@ -383,38 +624,43 @@ int mpb_create(const mpb_setup* su, mpb_handle** out) {
         for (int q = 0; q < su->n_materials; ++q) {
             const int id = su->materials[q].magnetic ? 128 + mm++ : nm++;
             if (nm > 128 || mm > 128) {
-                delete h;
+                mpb_destroy(h);
                 return fail_msg(MPB_EINVAL, "at most 128 magnetic and 128 non-magnetic materials");
             }
             remap[(size_t)q] = id;
             table[(size_t)id] = su->materials[q];
         }
     }
-    // material ids on the allocation layout, edge-padded (em.py:248-252)
-    const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
-    std::vector<uint8_t> ids((size_t)h->nentries, 0);
+    // material ids on the local field planes, edge-padded (em.py:248-252);
+    // magnetic cells of planes [lo, c1) (owned + the low ghost plane)
+    std::vector<uint8_t> ids((size_t)h->nloc, 0);
     std::vector<int2> cells;
+    std::vector<unsigned char> owned;
     int mx0 = nx, mx1 = 0;
-    for (int i = 0; i < F[0]; ++i)
+    for (int i = h->lo; i < h->hi; ++i)
         for (int j = 0; j < F[1]; ++j)
             for (int k = 0; k < F[2]; ++k) {
                 const int ci = std::min(i, nx - 1), cj = std::min(j, ny - 1),
                           ck = std::min(k, nz - 1);
-                const uint8_t id0 = su->cell_material[((size_t)ci * ny + cj) * nz + ck];
+                const uint8_t id0 =
+                    su->cell_material[((size_t)(ci - h->clo) * ny + cj) * nz + ck];
                 if (id0 >= su->n_materials) {
-                    delete h;
+                    mpb_destroy(h);
                     return fail_msg(MPB_EINVAL, "material id %d out of range", id0);
                 }
                 const uint8_t id = (uint8_t)remap[id0];
                 const int64_t f = (int64_t)j * F[2] + k;
-                ids[(size_t)(i * g.PP + f)] = id;
-                if (i < nx && j < ny && k < nz && table[id].magnetic) {
+                ids[(size_t)((i - h->lo) * g.PP + f)] = id;
+                if (i < nx && i < g.c1 && j < ny && k < nz && table[id].magnetic) {
                     cells.push_back(make_int2(i, (int)f));
+                    owned.push_back(i >= g.c0 ? 1 : 0);
                     mx0 = std::min(mx0, i);
                     mx1 = std::max(mx1, i + 1);
                 }
             }
     h->nmag = (int)cells.size();
+    for (unsigned char o : owned) h->nmag_owned += o;
+    h->any_magnetic = nranks == 1 ? (h->nmag > 0) : (su->any_magnetic != 0);
     if (h->nmag == 0) { mx0 = 0; mx1 = 0; }
     g.mx0 = mx0;
     g.mx1 = mx1;
@@ -424,25 +670,28 @@ int mpb_create(const mpb_setup* su, mpb_handle** out) {
     auto chk = [&](int r) { if (r && !rc) rc = r; };
     for (int p = 0; p < 2; ++p)
         for (int c = 0; c < 3; ++c) {
-            chk(dev_alloc(h, &h->E[p][c], (size_t)h->nentries));
-            chk(dev_alloc(h, &h->H[p][c], (size_t)h->nentries));
+            chk(dev_alloc(h, &h->E[p][c], (size_t)h->nloc));
+            chk(dev_alloc(h, &h->H[p][c], (size_t)h->nloc));
             chk(dev_alloc(h, &h->M[p][c], (size_t)(h->mplanes * g.PP)));
         }
-    chk(dev_alloc(h, &h->ids, (size_t)h->nentries));
+    chk(dev_alloc(h, &h->ids, (size_t)h->nloc));
     chk(dev_alloc(h, &h->mats, (size_t)MPB_MAX_MATERIALS));
     chk(dev_alloc(h, &h->magcells, (size_t)h->nmag));
+    chk(dev_alloc(h, &h->magowned, (size_t)h->nmag));
     chk(dev_alloc(h, &h->scratch, (size_t)h->nmag * 12));
     chk(dev_alloc(h, &h->st, 1));
     if (rc) { mpb_destroy(h); return rc; }
     CU(cudaMemcpy(h->ids, ids.data(), ids.size(), cudaMemcpyHostToDevice));
     CU(cudaMemcpy(h->mats, table.data(), sizeof(mpb_material) * table.size(),
                   cudaMemcpyHostToDevice));
-    if (h->nmag)
+    if (h->nmag) {
         CU(cudaMemcpy(h->magcells, cells.data(), sizeof(int2) * cells.size(),
                       cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(h->magowned, owned.data(), owned.size(), cudaMemcpyHostToDevice));
+    }
 
-    // cooperative fixup grid: co-resident blocks only
-    if (h->nmag) {
+    // cooperative fixup grid (single rank): co-resident blocks only
+    if (h->nmag && nranks == 1) {
         int per_sm = 0, sms = 0;
         CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_llg_fixup, 256, 0));
         CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
@@ -454,7 +703,7 @@ int mpb_create(const mpb_setup* su, mpb_handle** out) {
         if (rc) { mpb_destroy(h); return rc; }
     }
 
-    // source (em.py:276-282)
+    // source (em.py:276-282): only the owning rank injects
     for (int a = 0; a < 3; ++a) {
         if (su->src_loc[a] < 0 || su->src_loc[a] >= g.F[a]) {
             mpb_destroy(h);
@@ -462,6 +711,8 @@ int mpb_create(const mpb_setup* su, mpb_handle** out) {
         }
         h->src.pol[a] = su->src_pol[a];
     }
+    if (su->src_loc[0] < g.c0 || su->src_loc[0] >= g.c1)
+        h->src.pol[0] = h->src.pol[1] = h->src.pol[2] = 0.0;
     h->src.off = su->src_loc[0] * g.PP + (int64_t)su->src_loc[1] * F[2] + su->src_loc[2];
 
     // probes
@@ -480,15 +731,21 @@ int mpb_create(const mpb_setup* su, mpb_handle** out) {
             }
     }
     chk(dev_alloc(h, &h->probes, (size_t)std::max(1, h->nprobes)));
-    h->hostM.assign((size_t)3 * nx * ny * nz, 0.0);
+    h->hostM.assign((size_t)3 * (h->chi - h->clo) * ny * nz, 0.0);
     if (rc) { mpb_destroy(h); return rc; }
+    bool zero_id = true;
+    for (int q = 0; q < 128; ++q) zero_id = zero_id && su->nccl_id[q] == 0;
+    if (nranks > 1 && !zero_id) {   // all-zero id: in-process group (mpb_group_run)
+        ncclUniqueId id;
+        memcpy(&id, su->nccl_id, sizeof id);
+        ncclResult_t r = ncclCommInitRank(&h->comm, nranks, id, h->rank);
+        if (r != ncclSuccess) {
+            mpb_destroy(h);
+            return fail_msg(MPB_ECUDA, "ncclCommInitRank failed: %s", ncclGetErrorString(r));
+        }
+    }
     rc = reset_state(h);
     if (rc) { mpb_destroy(h); return rc; }
-    // probe table is (re)built by load_state; build it once for the zero state
-    const double* zf[6];
-    std::vector<double> zeros;
-    (void)zf; (void)zeros;
-    CU(cudaStreamSynchronize(h->stream));
     *out = h;
     return MPB_OK;
 }
@@ -509,6 +766,7 @@ void mpb_destroy(mpb_handle* h) {
     cudaFree(h->ids);
     cudaFree(h->mats);
     cudaFree(h->magcells);
+    cudaFree(h->magowned);
     cudaFree(h->scratch);
     cudaFree(h->st);
     cudaFree(h->probes);
@@ -516,37 +774,9 @@ void mpb_destroy(mpb_handle* h) {
     cudaFree(h->d_probe);
     cudaFree(h->d_iters);
     destroy_fused(h);
+    if (h->comm) ncclCommDestroy(h->comm);
     if (h->stream) cudaStreamDestroy(h->stream);
     delete h;
-}
-
-static int upload_probes(mpb_handle* h) {
-    const Geom& g = h->g;
-    std::vector<ProbeDesc> pd((size_t)std::max(1, h->nprobes));
-    const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
-    for (int p = 0; p < h->nprobes; ++p) {
-        const int comp = h->probe_comp[p];
-        const int* L = &h->probe_loc[3 * p];
-        const int64_t f = (int64_t)L[1] * g.F[2] + L[2];
-        ProbeDesc d{};
-        if (comp < MPB_COMP_HX) {
-            d.ptr0 = h->E[0][comp]; d.ptr1 = h->E[1][comp];
-            d.off = L[0] * g.PP + f;
-        } else if (comp < MPB_COMP_MX) {
-            d.ptr0 = h->H[0][comp - 3]; d.ptr1 = h->H[1][comp - 3];
-            d.off = L[0] * g.PP + f;
-        } else if (L[0] >= g.mx0 && L[0] < g.mx1) {
-            d.ptr0 = h->M[0][comp - 6]; d.ptr1 = h->M[1][comp - 6];
-            d.off = (int64_t)(L[0] - g.mx0) * g.PP + f;
-        } else {
-            d.ptr0 = d.ptr1 = nullptr;
-            d.constant = h->hostM[(((size_t)(comp - 6) * nx + L[0]) * ny + L[1]) * nz + L[2]];
-        }
-        pd[(size_t)p] = d;
-    }
-    CU(cudaMemcpy(h->probes, pd.data(), sizeof(ProbeDesc) * pd.size(),
-                  cudaMemcpyHostToDevice));
-    return MPB_OK;
 }
 
 int mpb_load_state(mpb_handle* h, const double* const fields[6], const double* m) {
@@ -556,13 +786,15 @@ int mpb_load_state(mpb_handle* h, const double* const fields[6], const double* m
     CU(cudaSetDevice(h->device));
     CU(cudaStreamSynchronize(h->stream));
     const size_t row = (size_t)g.FyFz * sizeof(double);
+    const int nplanes = h->hi - h->lo;
     for (int p = 0; p < 2; ++p)
         for (int c = 0; c < 6; ++c) {
             double* dst = c < 3 ? h->E[p][c] : h->H[p][c - 3];
-            CU(cudaMemcpy2D(dst, g.PP * sizeof(double), fields[c], row, row, h->Fx,
+            CU(cudaMemcpy2D(dst, g.PP * sizeof(double), fields[c], row, row, nplanes,
                             cudaMemcpyHostToDevice));
         }
-    const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
+    const int ny = g.n[1], nz = g.n[2];
+    const int ncl = h->chi - h->clo;
     memcpy(h->hostM.data(), m, h->hostM.size() * sizeof(double));
     if (h->mplanes) {
         std::vector<double> pk((size_t)(h->mplanes * g.PP), 0.0);
@@ -571,7 +803,7 @@ int mpb_load_state(mpb_handle* h, const double* const fields[6], const double* m
                 for (int j = 0; j < ny; ++j)
                     for (int k = 0; k < nz; ++k)
                         pk[(size_t)((i - g.mx0) * g.PP + (int64_t)j * g.F[2] + k)] =
-                            m[(((size_t)c * nx + i) * ny + j) * nz + k];
+                            m[(((size_t)c * ncl + (i - h->clo)) * ny + j) * nz + k];
             for (int p = 0; p < 2; ++p)
                 CU(cudaMemcpy(h->M[p][c], pk.data(), pk.size() * sizeof(double),
                               cudaMemcpyHostToDevice));
@@ -580,10 +812,7 @@ int mpb_load_state(mpb_handle* h, const double* const fields[6], const double* m
     h->parity = 0;
     int rc = upload_probes(h);
     if (rc) return rc;
-    rc = reset_state(h);
-    if (rc) return rc;
-    CU(cudaStreamSynchronize(h->stream));
-    return MPB_OK;
+    return reset_state(h);
 }
 
 int mpb_save_state(mpb_handle* h, double* const fields[6], double* m) {
@@ -594,12 +823,14 @@ int mpb_save_state(mpb_handle* h, double* const fields[6], double* m) {
     CU(cudaStreamSynchronize(h->stream));
     const size_t row = (size_t)g.FyFz * sizeof(double);
     const int p = h->parity;
+    const int nplanes = h->hi - h->lo;
     for (int c = 0; c < 6; ++c) {
         const double* src = c < 3 ? h->E[p][c] : h->H[p][c - 3];
-        CU(cudaMemcpy2D(fields[c], row, src, g.PP * sizeof(double), row, h->Fx,
+        CU(cudaMemcpy2D(fields[c], row, src, g.PP * sizeof(double), row, nplanes,
                         cudaMemcpyDeviceToHost));
     }
-    const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
+    const int ny = g.n[1], nz = g.n[2];
+    const int ncl = h->chi - h->clo;
     memcpy(m, h->hostM.data(), h->hostM.size() * sizeof(double));
     if (h->mplanes) {
         std::vector<double> pk((size_t)(h->mplanes * g.PP));
@@ -609,7 +840,7 @@ int mpb_save_state(mpb_handle* h, double* const fields[6], double* m) {
             for (int i = g.mx0; i < g.mx1; ++i)
                 for (int j = 0; j < ny; ++j)
                     for (int k = 0; k < nz; ++k)
-                        m[(((size_t)c * nx + i) * ny + j) * nz + k] =
+                        m[(((size_t)c * ncl + (i - h->clo)) * ny + j) * nz + k] =
                             pk[(size_t)((i - g.mx0) * g.PP + (int64_t)j * g.F[2] + k)];
         }
     }
@@ -740,14 +971,65 @@ int mpb_selftest_division(int32_t device, double d, const double* x, int64_t n,
     CU(cudaMemcpy(dx, x, sizeof(double) * n, cudaMemcpyHostToDevice));
     k_div_selftest<<<1184, 256>>>(dx, n, d, dm, db);
     CU(cudaGetLastError());
-    unsigned long long m = 0;
+    unsigned long long mm = 0;
     double bad = 0;
-    CU(cudaMemcpy(&m, dm, sizeof m, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(&mm, dm, sizeof mm, cudaMemcpyDeviceToHost));
     CU(cudaMemcpy(&bad, db, sizeof bad, cudaMemcpyDeviceToHost));
     cudaFree(dx); cudaFree(dm); cudaFree(db);
-    *mismatches = (int64_t)m;
+    *mismatches = (int64_t)mm;
     if (first_bad) *first_bad = bad;
     return MPB_OK;
+}
+
+int mpb_group_run(mpb_handle* const* hs, int32_t n, int64_t n0, int64_t nsteps,
+                  const double* src_vals, double* const* probe_out, int32_t* iters_out,
+                  mpb_failure* fail) {
+    g_err.clear();
+    if (fail) { fail->step = -1; fail->residual = 0; fail->iterations = 0; fail->kind = 0; }
+    if (!hs || n < 2 || n > kMaxGroup || nsteps < 0 || (nsteps && !src_vals))
+        return fail_msg(MPB_EINVAL, "bad arguments");
+    for (int r = 0; r < n; ++r) {
+        if (!hs[r] || hs[r]->nranks != n || hs[r]->rank != r || hs[r]->comm ||
+            hs[r]->device != hs[0]->device || hs[r]->parity != hs[0]->parity)
+            return fail_msg(MPB_EINVAL, "group: handles must be ranks 0..n-1 of one "
+                                        "decomposition on one device, created without NCCL");
+    }
+    CU(cudaSetDevice(hs[0]->device));
+    cudaStream_t s = hs[0]->stream;
+    std::vector<double*> dprobe((size_t)n, nullptr);
+    double* dsrc = nullptr;
+    int* diters = nullptr;
+    const int64_t cnt = std::max<int64_t>(nsteps, 1);
+    CU(cudaMalloc(&dsrc, cnt * sizeof(double)));
+    CU(cudaMalloc(&diters, cnt * sizeof(int) * n));
+    CU(cudaMemcpy(dsrc, src_vals, nsteps * sizeof(double), cudaMemcpyHostToDevice));
+    int rc = MPB_OK;
+    for (int r = 0; r < n && !rc; ++r) {
+        CU(cudaMalloc(&dprobe[(size_t)r], cnt * std::max(1, hs[r]->nprobes) * sizeof(double)));
+        rc = set_run_buffers(hs[r], n0, dsrc, dprobe[(size_t)r], diters + r * cnt);
+    }
+    for (int64_t t = 0; t < nsteps && !rc; ++t) {
+        rc = group_step(hs, n, hs[0]->parity, s);
+        for (int r = 0; r < n; ++r) hs[r]->parity ^= 1;
+    }
+    if (!rc) {
+        CU(cudaStreamSynchronize(s));
+        for (int r = 0; r < n; ++r)
+            if (probe_out && probe_out[r] && hs[r]->nprobes)
+                CU(cudaMemcpy(probe_out[r], dprobe[(size_t)r],
+                              nsteps * hs[r]->nprobes * sizeof(double), cudaMemcpyDeviceToHost));
+        if (iters_out) CU(cudaMemcpy(iters_out, diters, nsteps * sizeof(int), cudaMemcpyDeviceToHost));
+        mpb_failure fl;
+        rc = read_failure(hs[0], &fl);
+        if (rc == MPB_ESTEP) {
+            if (fail) *fail = fl;
+            fail_msg(MPB_ESTEP, "LLG fixed point failed at step %lld", (long long)fl.step);
+        }
+    }
+    cudaFree(dsrc);
+    cudaFree(diters);
+    for (double* p : dprobe) cudaFree(p);
+    return rc;
 }
 
 int64_t mpb_launch_count(mpb_handle* h) { return h ? h->launches_last : 0; }

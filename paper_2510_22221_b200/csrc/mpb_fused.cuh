@@ -68,7 +68,7 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
         return fail_msg(MPB_EINVAL, "fused sweep staging (%zu B) exceeds shared memory",
                         fs->smem);
     // x-chunks: ~8 waves of one CTA per SM, chunks of >= 24 planes
-    const int Fx = g.F[0];
+    const int Fx = g.c1 - g.c0;                      // owned planes of this rank
     int waves = 16;
     if (const char* e = getenv("MPB_SWEEP_WAVES")) waves = std::max(1, atoi(e));
     const int want = std::max(1, (waves * sms + sc.tiles - 1) / sc.tiles);
@@ -87,13 +87,16 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
         CU(cudaMemcpy(cells.data(), h->magcells, sizeof(int2) * cells.size(),
                       cudaMemcpyDeviceToHost));
         keys.reserve(cells.size() * 4);
+        auto add = [&](int i, int64_t f) {
+            if (i >= g.c0 && i < g.c1) keys.push_back((int64_t)i * g.FyFz + f);
+        };
         for (const int2& c : cells) {
             const int i = c.x, f = c.y;
             const int j = f / Fz, k = f - j * Fz;
-            keys.push_back((int64_t)i * g.FyFz + f);
-            if (g.act[0] && i + 1 < g.F[0]) keys.push_back((int64_t)(i + 1) * g.FyFz + f);
-            if (g.act[1] && j + 1 < g.F[1]) keys.push_back((int64_t)i * g.FyFz + f + Fz);
-            if (g.act[2] && k + 1 < g.F[2]) keys.push_back((int64_t)i * g.FyFz + f + 1);
+            add(i, f);
+            if (g.act[0] && i + 1 < g.F[0]) add(i + 1, f);
+            if (g.act[1] && j + 1 < g.F[1]) add(i, f + Fz);
+            if (g.act[2] && k + 1 < g.F[2]) add(i, f + 1);
         }
         std::sort(keys.begin(), keys.end());
         keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
@@ -110,10 +113,12 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
     if (g.act[2] && (g.faces[4] != MPB_FACE_PMC || g.faces[5] != MPB_FACE_PMC)) {
         std::set<int> jset, iset;
         if (g.act[1]) for (int j : {0, 1, g.n[1] - 1, g.n[1]}) jset.insert(j);
-        if (g.act[0]) for (int i : {0, 1, g.n[0] - 1, g.n[0]}) iset.insert(i);
+        if (g.act[0])
+            for (int i : {0, 1, g.n[0] - 1, g.n[0]})
+                if (i >= g.c0 && i < g.c1) iset.insert(i);
         std::vector<int3> lines;
         for (int j : jset)
-            for (int i = 0; i < g.F[0]; ++i) lines.push_back(make_int3(0, i, j));
+            for (int i = g.c0; i < g.c1; ++i) lines.push_back(make_int3(0, i, j));
         for (int i : iset)
             for (int j = 0; j < g.F[1]; ++j) lines.push_back(make_int3(1, i, j));
         fs->nzlines = (int)lines.size();
@@ -130,7 +135,7 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
 int launch_zfix(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s) {
     FusedState* fs = fused_of(h);
     if (!fs->nzlines) return MPB_OK;
-    k_zfix<<<(fs->nzlines + 255) / 256, 256, 0, s>>>(g, b, h->mats, h->ids, fs->zlines,
+    k_zfix<<<(fs->nzlines + 255) / 256, 256, 0, s>>>(g, b, h->mats, ids_view(h), fs->zlines,
                                                      fs->nzlines, h->st);
     return MPB_OK;
 }
@@ -149,9 +154,9 @@ void destroy_fused(mpb_handle* h) {
 int launch_fused(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s) {
     FusedState* fs = fused_of(h);
     switch (fs->V) {
-        case 4: k_sweep<4><<<fs->grid, kSweepThreads, fs->smem, s>>>(g, b, h->mats, h->ids, h->st, fs->sc); break;
-        case 2: k_sweep<2><<<fs->grid, kSweepThreads, fs->smem, s>>>(g, b, h->mats, h->ids, h->st, fs->sc); break;
-        default: k_sweep<1><<<fs->grid, kSweepThreads, fs->smem, s>>>(g, b, h->mats, h->ids, h->st, fs->sc); break;
+        case 4: k_sweep<4><<<fs->grid, kSweepThreads, fs->smem, s>>>(g, b, h->mats, ids_view(h), h->st, fs->sc); break;
+        case 2: k_sweep<2><<<fs->grid, kSweepThreads, fs->smem, s>>>(g, b, h->mats, ids_view(h), h->st, fs->sc); break;
+        default: k_sweep<1><<<fs->grid, kSweepThreads, fs->smem, s>>>(g, b, h->mats, ids_view(h), h->st, fs->sc); break;
     }
     return MPB_OK;
 }
@@ -159,7 +164,7 @@ int launch_fused(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s) {
 int launch_deferred(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s) {
     FusedState* fs = fused_of(h);
     if (!fs->ndefer) return MPB_OK;
-    k_edefer<<<(fs->ndefer + 255) / 256, 256, 0, s>>>(g, b, h->mats, h->ids, fs->defer,
+    k_edefer<<<(fs->ndefer + 255) / 256, 256, 0, s>>>(g, b, h->mats, ids_view(h), fs->defer,
                                                     fs->ndefer, h->st);
     return MPB_OK;
 }

@@ -31,7 +31,7 @@ __device__ __forceinline__ void cta_stats_flush(const CtaLlgStats& s, int max_it
         if (v) atomicMax(&st->hist[r], v);
     }
     if (threadIdx.x == 0) {
-        atomicMin(&st->rc_min, s.rc[0]);
+        atomicMax(&st->rc_negmin, -s.rc[0]);
         atomicMax(&st->rc_max, s.rc[1]);
     }
 }
@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(256) k_llg_fixup(Geom g, Bufs b,
                                                    MagScratch scr, StepState* st) {
     __shared__ unsigned long long red[32];
     if (st->fail) return;
-    const int rmin = st->rc_min, rmax = st->rc_max;
+    const int rmin = -st->rc_negmin, rmax = st->rc_max;
     if (rmin == rmax && rmax <= g.max_iters) {
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             double fr; int fi, fk;
@@ -286,6 +286,111 @@ __global__ void __launch_bounds__(256) k_llg_fixup(Geom g, Bufs b,
 }
 
 // ---------------------------------------------------------------------------
+// Multi-rank LLG settlement (no grid-wide barrier across GPUs).  After the
+// sweep, hist and (rc_max, -rc_min) are all-reduced (max) over the ranks.
+//  * uniform: every cell stopped at the same R -> replay the stop rule.
+//  * otherwise: every cell (owned + ghost-plane copies) is recomputed from
+//    scratch to R' = min(R, max_iters) (k_llg_topup), the owned residuals of
+//    iterates 1..R' are all-reduced into hist2, and k_llg_decide replays the
+//    rule on hist2.  A cell that had stopped earlier cannot make hist2[r]
+//    <= tol for r < R' (the cell with r_c = R' is still > tol there), so the
+//    rule stops at R' unless the global residual is non-monotone at R'
+//    (a cell back above tol) -- then the step is flagged (kind 3) instead of
+//    silently diverging from the reference.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_llg_topup(Geom g, Bufs b,
+                                                   const mpb_material* __restrict__ mats,
+                                                   const uint8_t* __restrict__ ids,
+                                                   const int2* __restrict__ cells,
+                                                   const unsigned char* __restrict__ owned,
+                                                   int ncells, StepState* st) {
+    __shared__ unsigned long long sh[MPB_MAX_ITERS_CAP + 2];
+    if (st->fail) return;
+    const int rmin = -st->rc_negmin, rmax = st->rc_max;
+    if (rmin == rmax && rmax <= g.max_iters) return;       // uniform case
+    const int R = min(rmax, g.max_iters);
+    for (int r = threadIdx.x; r <= R + 1; r += blockDim.x) sh[r] = 0ull;
+    __syncthreads();
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q < ncells) {
+        const int i = cells[q].x, f = cells[q].y;
+        const int64_t o = i * g.PP + f;
+        const int64_t om = (int64_t)(i - g.mx0) * g.PP + f;
+        LlgCell s;
+        const Curl3 c = curl_e_at(g, b.Ea, o, g.PP, g.F[2], true, true, true);
+        for (int k = 0; k < 3; ++k) { s.Hn[k] = b.Ha[k][o]; s.Mn[k] = b.Ma[k][om]; }
+        s.cE[0] = c.x; s.cE[1] = c.y; s.cE[2] = c.z;
+        llg_setup(s, mats[ids[o]]);
+        double Hr[3] = {s.Hn[0], s.Hn[1], s.Hn[2]};
+        double Mr[3] = {s.Mn[0], s.Mn[1], s.Mn[2]};
+        const bool own = owned[q] != 0;
+        for (int r = 1; r <= R; ++r) {
+            const double res = llg_iterate(s, g.coef_h, Hr, Mr);
+            if (own) atomicMax(&sh[r], dbits(res));
+        }
+        for (int k = 0; k < 3; ++k) b.Hb[k][o] = Hr[k];
+        if (own)
+            for (int k = 0; k < 3; ++k) b.Mb[k][om] = Mr[k];
+    }
+    __syncthreads();
+    for (int r = 1 + threadIdx.x; r <= R; r += blockDim.x)
+        if (sh[r]) atomicMax(&st->hist2[r], sh[r]);
+}
+
+// In-process multi-rank emulation (mpb_group_run): the all-reduce(max) of
+// the NCCL path over the ranks' states, one block.
+constexpr int kMaxGroup = 16;
+struct StatePtrs {
+    StepState* s[kMaxGroup];
+    int n;
+};
+
+__global__ void k_group_reduce(StatePtrs sp, int max_iters, int mode) {
+    for (int r = 1 + threadIdx.x; r <= max_iters + 1; r += blockDim.x) {
+        if (r <= max_iters) {
+            unsigned long long m = 0ull;
+            for (int q = 0; q < sp.n; ++q) {
+                const unsigned long long v = mode == 0 ? sp.s[q]->hist[r] : sp.s[q]->hist2[r];
+                m = v > m ? v : m;
+            }
+            for (int q = 0; q < sp.n; ++q) {
+                if (mode == 0) sp.s[q]->hist[r] = m;
+                else sp.s[q]->hist2[r] = m;
+            }
+        } else if (mode == 0) {
+            int a = sp.s[0]->rc_max, b = sp.s[0]->rc_negmin;
+            for (int q = 1; q < sp.n; ++q) {
+                a = max(a, sp.s[q]->rc_max);
+                b = max(b, sp.s[q]->rc_negmin);
+            }
+            for (int q = 0; q < sp.n; ++q) { sp.s[q]->rc_max = a; sp.s[q]->rc_negmin = b; }
+        }
+    }
+}
+
+__global__ void k_llg_decide(Geom g, StepState* st) {
+    if (threadIdx.x != 0 || st->fail) return;
+    const int rmin = -st->rc_negmin, rmax = st->rc_max;
+    double fr = 0.0; int fi = 0, fk = 0, r;
+    if (rmax == 0) return;                                 // no magnetic cell anywhere
+    if (rmin == rmax && rmax <= g.max_iters) {
+        r = llg_decide(st->hist, rmax, g.max_iters, g.tol, &fr, &fi, &fk);
+    } else {
+        const int R = min(rmax, g.max_iters);
+        r = llg_decide(st->hist2, R, g.max_iters, g.tol, &fr, &fi, &fk);
+        st->fixup_ran = 1;
+        if (r > 0 && r != R) { r = -1; }
+        if (r < 0) { fr = bitsd(st->hist2[R]); fi = R; fk = 3; r = 0; }
+    }
+    if (r > 0) {
+        st->rstar = r;
+    } else {
+        st->fail = 1; st->fail_step = st->step; st->fail_res = fr;
+        st->fail_it = fi; st->fail_kind = fk;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Walls, one launch per face in the order x0,x1,y0,y1,z0,z1 (em.py:324-359).
 // MUR1 reads the pre-update planes straight from the read buffer Ea (the
 // reference copies them before the update, em.py:306-321).
@@ -298,10 +403,12 @@ __global__ void __launch_bounds__(256) k_wall(Geom g, Bufs b,
     const int axis = face >> 1, side = face & 1;
     const int u = axis == 0 ? 1 : 0;          // the two in-plane axes
     const int w = axis == 2 ? 1 : 2;
-    const int nu = g.F[u], nw = g.F[w];
+    // x is the slab axis: y/z faces cover the owned planes only
+    const int u0 = u == 0 ? g.c0 : 0;
+    const int nu = u == 0 ? g.c1 - g.c0 : g.F[u], nw = g.F[w];
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= (int64_t)nu * nw) return;
-    const int iu = (int)(t / nw), iw = (int)(t - (int64_t)iu * nw);
+    const int iu = u0 + (int)(t / nw), iw = (int)(t - (int64_t)(iu - u0) * nw);
     const int64_t stride[3] = {g.PP, g.F[2], 1};
     const int wall = side == 0 ? 0 : g.n[axis];
     const int inner = side == 0 ? 1 : g.n[axis] - 1;
@@ -358,7 +465,7 @@ __global__ void __launch_bounds__(256) k_finish(Geom g, Bufs b, SourceDesc src,
         if (record_iters) st->iters_out[row] = st->rstar;
         st->rstar = 0;
         st->fixup_ran = 0;
-        st->rc_min = 0x7fffffff;
+        st->rc_negmin = -0x7fffffff;
         st->rc_max = 0;
         st->local = row + 1;
         st->step = st->step + 1;

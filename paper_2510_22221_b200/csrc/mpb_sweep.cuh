@@ -198,8 +198,8 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
     const int f0 = tile * sc.T;
     const int f1 = min(f0 + sc.T, g.FyFz);
     const int Fx = g.F[0];
-    const int i0 = chunk * sc.chunk;
-    const int i1 = min(i0 + sc.chunk, Fx);
+    const int i0 = g.c0 + chunk * sc.chunk;          // owned planes [c0, c1)
+    const int i1 = min(i0 + sc.chunk, g.c1);
     if (i0 >= i1) return;
     const int pstart = i0 > 0 ? i0 - 1 : 0;
     // last plane whose stage is needed: i1 (E only, for dEz/dx, dEy/dx of
@@ -409,6 +409,16 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
                     if (j < ny && k < nz) b.Hb[0][o] = hx;
                     if (cp && k < nz) b.Hb[1][o] = hy;
                     if (cp && j < ny) b.Hb[2][o] = hz;
+                } else if (p == g.c0 - 1) {
+                    // low ghost plane of a slab: its H^{n+1} is read by k_edefer
+                    // (x-backward difference at plane c0) before the exchange
+                    // delivers the owner's copy (identical values)
+                    const int j = fz_div((uint32_t)f, sc.fz_magic);
+                    const int k = f - j * Fz;
+                    const uint32_t o = (uint32_t)base + (uint32_t)f;
+                    if (j < ny && k < nz) b.Hb[0][o] = hx;
+                    if (k < nz) b.Hb[1][o] = hy;
+                    if (j < ny) b.Hb[2][o] = hz;
                 }
                 hy_prev[v] = hy;
                 hz_prev[v] = hz;
@@ -422,7 +432,7 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
             if (v) atomicMax(&st->hist[r], v);
         }
         if (tid == 0) {
-            atomicMin(&st->rc_min, s_rc[0]);
+            atomicMax(&st->rc_negmin, -s_rc[0]);
             atomicMax(&st->rc_max, s_rc[1]);
         }
     }

@@ -118,16 +118,25 @@ class DeviceRun:
 
     def __init__(self, grid, materials, boundaries, source_loc, source_pol,
                  probes, llg_params, dt: float, device: int = 0,
-                 kernel_variant: int = 0, graph_steps: int = 0):
+                 kernel_variant: int = 0, graph_steps: int = 0, slab=None):
+        """``slab``: None (whole grid on one GPU) or a ``parallel.Slab``
+        (multi-rank x-slab); ``materials`` then covers the slab's cell
+        planes incl. ghosts (``Slab.cell_range``), ``grid`` is global."""
         self.lib = N.load_library()
         self.grid = grid
         self.n = grid.cell_shape
         self.fs = grid.field_shape
+        self.slab = slab
+        if slab is not None:
+            f0, f1 = slab.field_range
+            c0, c1 = slab.cell_range
+            self.fs = (f1 - f0,) + tuple(self.fs[1:])
+            self.n = (c1 - c0,) + tuple(self.n[1:])
         self.probes = list(probes)
         ids, table = material_table(materials, dt, grid.spacings)
         self._keep = [ids, table]
         su = N.Setup()
-        su.n[:] = list(self.n)
+        su.n[:] = list(grid.cell_shape)          # global grid; slabs carry ranges
         su.d[:] = list(grid.spacings)
         su.dt = dt
         su.coef_h = dt / CONSTANTS.mu0
@@ -153,6 +162,14 @@ class DeviceRun:
         su.device = device
         su.kernel_variant = kernel_variant
         su.graph_steps = graph_steps
+        if slab is None:
+            su.nranks, su.rank, su.x_lo, su.x_hi = 1, 0, 0, grid.nx
+            su.any_magnetic = int(np.count_nonzero(np.asarray(materials.Ms) > 0) > 0)
+        else:
+            su.nranks, su.rank = slab.nranks, slab.rank
+            su.x_lo, su.x_hi = slab.x_lo, slab.x_hi
+            su.any_magnetic = int(slab.any_magnetic)
+            su.nccl_id[:] = list(slab.nccl_id)
         h = C.c_void_p()
         N.check(self.lib.mpb_create(C.byref(su), C.byref(h)))
         self.h = h

@@ -107,7 +107,9 @@ def source_values(src: em.SourceSpec, dt: float, start: int, stop: int) -> np.nd
                     dtype=np.float64)
 
 
-def _device_run(config, materials, keys, device: int = 0, **kw) -> DeviceRun:
+def _device_run_args(config, keys) -> dict:
+    """Validate probes/walls/source like the reference would at run time and
+    return the device-facing source and wall arguments."""
     fs = config.grid.field_shape
     pol = config.source.polarization
     loc = config.source.location
@@ -126,8 +128,14 @@ def _device_run(config, materials, keys, device: int = 0, **kw) -> DeviceRun:
     for face, axis in (("x0", 0), ("x1", 0), ("y0", 1), ("y1", 1), ("z0", 2), ("z1", 2)):
         if getattr(b, face) == em.MUR1 and not config.grid.active_axes[axis]:
             raise ValueError(f"MUR1 on collapsed axis face {face}")
-    return DeviceRun(config.grid, materials, b, loc, pol, keys, config.llg_params,
-                     config.dt, device=device, **kw)
+    return {"source_loc": loc, "source_pol": pol, "boundaries": b}
+
+
+def _device_run(config, materials, keys, device: int = 0, **kw) -> DeviceRun:
+    a = _device_run_args(config, keys)
+    return DeviceRun(config.grid, materials, a["boundaries"], a["source_loc"],
+                     a["source_pol"], keys, config.llg_params, config.dt,
+                     device=device, **kw)
 
 
 def run(config: SimConfig, bias: float | None = None, resume: dict | None = None,

@@ -1,0 +1,32 @@
+"""Multi-rank x-slab decomposition, emulated on one GPU (mpb_group_run):
+the same kernels and boundary-plane movement as the NCCL path must give
+results bit-identical to the reference goldens (SURVEY 8e correctness gate:
+P-rank == 1-rank, bitwise)."""
+
+import numpy as np
+import pytest
+
+from paper_2510_22221_b200 import parallel
+from tests.golden.cases import CASES, build, mirror_namespace
+from tests.golden_io import load
+
+pytestmark = pytest.mark.gpu
+
+SPLITS = [("mixed3d", 2), ("mixed3d", 3), ("allmur3d", 2), ("allmur3d", 5),
+          ("pec_block", 4), ("zwall_magnet", 2), ("zwall_magnet", 3), ("thin", 3),
+          ("plane2d", 2), ("xline1d", 4), ("bias3d", 2)]
+
+
+@pytest.mark.parametrize("name,nranks", SPLITS)
+def test_slab_group_matches_reference_golden(name, nranks):
+    case = CASES[name]
+    g = load(name)
+    cfg = build(case, mirror_namespace())
+    fields, M, probes, its = parallel.run_group(cfg, nranks, bias=case.get("bias"))
+    assert fields is not None, f"step failure: {its}"
+    for k, v in g["fields"].items():
+        got = M if k == "M" else fields[k]
+        assert np.array_equal(got, v), (k, np.max(np.abs(got - v)))
+    assert np.array_equal(its, g["iterations"])
+    for key, v in g["probes"].items():
+        assert np.array_equal(probes[key], v), key
