@@ -115,7 +115,7 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(inside)}
 
 
-def synthetic_state(cfg, kind: str):
+def synthetic_state(fs, kind: str):
     """Initial E, H for the benchmark.
 
     "random": a mid-run-like state -- every entry carries a nonzero field
@@ -123,7 +123,7 @@ def synthetic_state(cfg, kind: str):
     fresh run is exact zeros almost everywhere for thousands of steps).
     "zero": the reference's own initial state.
     """
-    fs = cfg.grid.field_shape
+    fs = tuple(fs)
     if kind == "zero":
         z = np.zeros(fs)
         return {n: z for n in ("Ex", "Ey", "Ez", "Hx", "Hy", "Hz")}
@@ -134,6 +134,45 @@ def synthetic_state(cfg, kind: str):
         scale = 1e3 * (1.0 + 0.1 * q) if n[0] == "E" else 2.65 * (1.0 + 0.1 * q)
         out[n] = np.roll(base, q, axis=-1) * scale
     return out
+
+
+def weak_scaled_slab(cfg, keys, world, rank, local, args):
+    """Weak scaling (SURVEY 8e / BASELINE C4): the global grid is the C4
+    geometry repeated along x, (nx * world) x ny x nz; rank r owns the x-slab
+    [nx r, nx (r+1)) and exchanges boundary planes with its neighbours over
+    NCCL every step.  Source and probes live on rank 0's slab."""
+    import torch.distributed as dist
+    from dataclasses import replace
+
+    from paper_2510_22221_b200 import parallel
+    from paper_2510_22221_b200.engine import DeviceRun
+    from paper_2510_22221_b200.grid import GridSpec, initial_magnetization
+    from paper_2510_22221_b200.sim import _device_run_args
+
+    g = cfg.grid
+    ggrid = GridSpec(g.nx * world, g.ny, g.nz, g.dx, g.dy, g.dz)
+    gcfg = replace(cfg, grid=ggrid, probes=())
+    nccl_id = parallel.nccl_unique_id(dist)
+    slab = replace(parallel.make_slabs(ggrid.nx, world, True)[rank], nccl_id=nccl_id)
+    c0, c1 = slab.cell_range
+    period = np.arange(c0, c1) % g.nx          # C4 repeated along x
+
+    class Slab:
+        pass
+    mats = Slab()
+    for name in ("sigma", "eps_r", "Ms", "alpha", "gamma_e"):
+        setattr(mats, name, np.ascontiguousarray(np.asarray(getattr(cfg.materials, name))[period]))
+    mats.Hbias = np.ascontiguousarray(np.asarray(cfg.materials.Hbias)[:, period])
+    mats.shape = mats.Ms.shape
+    mats.magnetic_mask = mats.Ms > 0.0
+    a = _device_run_args(gcfg, keys)
+    dev = DeviceRun(ggrid, mats, a["boundaries"], a["source_loc"], a["source_pol"], keys,
+                    cfg.llg_params, cfg.dt, device=local, kernel_variant=args.variant,
+                    slab=slab)
+    f0, f1 = slab.field_range
+    st = synthetic_state((f1 - f0,) + tuple(ggrid.field_shape[1:]), args.init)
+    dev.load_state(st, initial_magnetization(mats))
+    return dev
 
 
 def cpu_oracle_sample(cfg_name: str, steps: int):
@@ -224,9 +263,13 @@ def main() -> None:
     f_mag = mag / cells
     keys = [(p[0], (p[1], p[2], p[3])) for p in cfg.probes]
     keys = list(dict.fromkeys(keys))
-    dev = sim._device_run(cfg, cfg.materials, keys, device=local,
-                          kernel_variant=args.variant)
-    dev.load_state(synthetic_state(cfg, args.init), initial_magnetization(cfg.materials))
+    if world == 1:
+        dev = sim._device_run(cfg, cfg.materials, keys, device=local,
+                              kernel_variant=args.variant)
+        dev.load_state(synthetic_state(cfg.grid.field_shape, args.init),
+                       initial_magnetization(cfg.materials))
+    else:
+        dev = weak_scaled_slab(cfg, keys, world, rank, local, args)
     total = args.warmup + args.steps
     src = torch.tensor(sim.source_values(cfg.source, cfg.dt, 0, total),
                        dtype=torch.float64, device="cuda")

@@ -575,6 +575,7 @@ int mpb_create(const mpb_setup* su, mpb_handle** out) {
     h->device = su->device;
     h->variant = su->kernel_variant;
     h->graph_steps = su->graph_steps > 0 ? su->graph_steps : kDefaultGraphSteps;
+    if (nranks > 1) h->graph_steps = 1;   // NCCL steps are enqueued eagerly
     h->nranks = nranks;
     h->rank = nranks == 1 ? 0 : su->rank;
     CU(cudaSetDevice(h->device));
