@@ -8,6 +8,7 @@ namespace {
 struct FusedState {
     SweepCfg sc{};
     int V = 2;
+    bool F3 = true;
     int grid = 0;
     size_t smem = 0;
     int2* defer = nullptr;
@@ -18,9 +19,9 @@ struct FusedState {
 
 FusedState* fused_of(mpb_handle* h) { return reinterpret_cast<FusedState*>(h->fused); }
 
-template <int V>
+template <int V, bool F3>
 int set_smem_attr(size_t smem) {
-    CU(cudaFuncSetAttribute(k_sweep<V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CU(cudaFuncSetAttribute(k_sweep<V, F3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)smem));
     return MPB_OK;
 }
@@ -77,8 +78,23 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
     sc.chunk = (Fx + sc.nchunks - 1) / sc.nchunks;
     sc.nchunks = (Fx + sc.chunk - 1) / sc.chunk;
     fs->grid = sc.tiles * sc.nchunks;
-    int rc = fs->V == 4 ? set_smem_attr<4>(fs->smem)
-                        : (fs->V == 2 ? set_smem_attr<2>(fs->smem) : set_smem_attr<1>(fs->smem));
+    fs->F3 = g.act[0] && g.act[1] && g.act[2];
+    int rc;
+    if (fs->F3)
+        rc = fs->V == 4 ? set_smem_attr<4, true>(fs->smem)
+                        : (fs->V == 2 ? set_smem_attr<2, true>(fs->smem) : set_smem_attr<1, true>(fs->smem));
+    else
+        rc = fs->V == 4 ? set_smem_attr<4, false>(fs->smem)
+                        : (fs->V == 2 ? set_smem_attr<2, false>(fs->smem) : set_smem_attr<1, false>(fs->smem));
+    if (rc) return rc;
+    {   // reciprocals of the spacings, computed once on the device
+        double* dr = nullptr;
+        CU(cudaMalloc(&dr, 3 * sizeof(double)));
+        k_recips<<<1, 1>>>(g.d[0], g.d[1], g.d[2], dr);
+        CU(cudaGetLastError());
+        CU(cudaMemcpy(sc.rd, dr, 3 * sizeof(double), cudaMemcpyDeviceToHost));
+        cudaFree(dr);
+    }
     if (rc) return rc;
     // deferred E entries: {c, c+x, c+y, c+z} over magnetic cells
     std::vector<int64_t> keys;
@@ -153,11 +169,19 @@ void destroy_fused(mpb_handle* h) {
 
 int launch_fused(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s) {
     FusedState* fs = fused_of(h);
-    switch (fs->V) {
-        case 4: k_sweep<4><<<fs->grid, kSweepThreads, fs->smem, s>>>(g, b, h->mats, ids_view(h), h->st, fs->sc); break;
-        case 2: k_sweep<2><<<fs->grid, kSweepThreads, fs->smem, s>>>(g, b, h->mats, ids_view(h), h->st, fs->sc); break;
-        default: k_sweep<1><<<fs->grid, kSweepThreads, fs->smem, s>>>(g, b, h->mats, ids_view(h), h->st, fs->sc); break;
+#define MPB_LAUNCH(VV, FF)                                                              \
+    k_sweep<VV, FF><<<fs->grid, kSweepThreads, fs->smem, s>>>(g, b, h->mats, ids_view(h), \
+                                                              h->st, fs->sc)
+    if (fs->F3) {
+        if (fs->V == 4) MPB_LAUNCH(4, true);
+        else if (fs->V == 2) MPB_LAUNCH(2, true);
+        else MPB_LAUNCH(1, true);
+    } else {
+        if (fs->V == 4) MPB_LAUNCH(4, false);
+        else if (fs->V == 2) MPB_LAUNCH(2, false);
+        else MPB_LAUNCH(1, false);
     }
+#undef MPB_LAUNCH
     return MPB_OK;
 }
 

@@ -85,7 +85,14 @@ struct SweepCfg {
     int ring_offset;    // bytes of dynamic smem before the ring (LLG history)
     int nmat;           // entries of the material table
     int fastdiv;        // spacings within [2^-40, 2^10]: range-guarded divisions
+    double rd[3];       // recip_of(d[a]) evaluated on the device at setup
 };
+
+__global__ void k_recips(double dx, double dy, double dz, double* out) {
+    out[0] = recip_of(dx);
+    out[1] = recip_of(dy);
+    out[2] = recip_of(dz);
+}
 
 constexpr int kSweepThreads = 512;
 constexpr int kSlots = 3;
@@ -143,7 +150,8 @@ struct HCtx {
 __device__ __forceinline__ void h_entry(const Geom& g, const HCtx& c, int e, int j, int k,
                                         bool cellplane, int Fz, double ry, double rz,
                                         double rx, double& cx, double& cy, double& cz,
-                                        bool& vx, bool& vy, bool& vz, bool g_fastdiv) {
+                                        bool& vx, bool& vy, bool& vz, bool g_fastdiv,
+                                        bool ax, bool ay, bool az) {
     vx = j < g.n[1] && k < g.n[2];
     vy = cellplane && k < g.n[2];
     vz = cellplane && j < g.n[1];
@@ -172,12 +180,12 @@ __device__ __forceinline__ void h_entry(const Geom& g, const HCtx& c, int e, int
     }
     // em.py:130-138 accumulation order, collapsed axes omitted
     cx = 0.0; cy = 0.0; cz = 0.0;
-    if (g.act[1]) { cx = cx + q0; cz = cz - q1; }
-    if (g.act[2]) { cx = cx - q2; cy = cy + q3; }
-    if (g.act[0]) { cy = cy - q4; cz = cz + q5; }
+    if (ay) { cx = cx + q0; cz = cz - q1; }
+    if (az) { cx = cx - q2; cy = cy + q3; }
+    if (ax) { cy = cy - q4; cz = cz + q5; }
 }
 
-template <int V>
+template <int V, bool F3>
 __global__ void __launch_bounds__(kSweepThreads, 1)
 k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
         const uint8_t* __restrict__ gids, StepState* st, SweepCfg sc) {
@@ -204,7 +212,9 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
     const int pstart = i0 > 0 ? i0 - 1 : 0;
     // last plane whose stage is needed: i1 (E only, for dEz/dx, dEy/dx of
     // plane i1-1) when it exists and x is active
-    const int plast = (g.act[0] && i1 < Fx) ? i1 : i1 - 1;
+    // F3: every axis active (3D grids) -- axis tests fold away at compile time
+    const bool ax = F3 || g.act[0], ay = F3 || g.act[1], az = F3 || g.act[2];
+    const int plast = (ax && i1 < Fx) ? i1 : i1 - 1;
     const int hlo = max(0, f0 - sc.hl);
     const int ehi = min(g.FyFz, f1 + sc.eh);
     const int a0 = hlo & ~1;                         // 16-byte aligned starts
@@ -258,15 +268,15 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
     if (tid == 0)
         for (int p = pstart; p <= plast && p < pstart + kSlots; ++p) issue(p);
 
-    const double ry = g.act[1] ? recip_of(g.d[1]) : 1.0;
-    const double rz = g.act[2] ? recip_of(g.d[2]) : 1.0;
-    const double rx = g.act[0] ? recip_of(g.d[0]) : 1.0;
+    // reciprocals of the spacings: recip_of() evaluated once at setup on the
+    // device (identical bits); passing them keeps MUFU + 5 DFMA out of the loop
+    const double rx = sc.rd[0], ry = sc.rd[1], rz = sc.rd[2];
     const int Fz = g.F[2];
     const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
     // collapsed axes: their (unused) quotients must not trip the guard
-    const bool fastdiv = sc.fastdiv != 0 && g.act[0] && g.act[1] && g.act[2];
-    const bool zw0 = g.act[2] && g.faces[4] != MPB_FACE_PMC;
-    const bool zw1 = g.act[2] && g.faces[5] != MPB_FACE_PMC;
+    const bool fastdiv = sc.fastdiv != 0 && ax && ay && az;
+    const bool zw0 = az && g.faces[4] != MPB_FACE_PMC;
+    const bool zw1 = az && g.faces[5] != MPB_FACE_PMC;
     const bool z0pec = g.faces[4] == MPB_FACE_PEC, z1pec = g.faces[5] == MPB_FACE_PEC;
     const bool pmc_x0 = g.faces[0] == MPB_FACE_PMC, pmc_x1 = g.faces[1] == MPB_FACE_PMC;
     const bool pmc_y0 = g.faces[2] == MPB_FACE_PMC, pmc_y1 = g.faces[3] == MPB_FACE_PMC;
@@ -278,7 +288,7 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
 
     for (int p = pstart; p <= i1 - 1; ++p) {
         const int s = slot(p);
-        const bool xnext = g.act[0] && p < nx;           // plane p+1 used by dx terms
+        const bool xnext = ax && p < nx;                 // plane p+1 used by dx terms
         const int s1 = slot(p + 1);
         if (tid == 0) {
             mbar_wait(&bars[s], ((p - pstart) / kSlots) & 1);
@@ -293,7 +303,7 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
                 sH(s, 0), sH(s, 1), sH(s, 2)};
         const unsigned char* ids = sI(s);
         const bool emit = p >= i0;
-        const bool cellplane = p < nx || !g.act[0];
+        const bool cellplane = p < nx || !ax;
 
         // ---- H^{n+1}(p, g) for g in [hlo, f1), in place --------------------
         for (int gg = hlo + tid; gg < f1; gg += kSweepThreads) {
@@ -302,7 +312,8 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
             const int e = gg - a0;
             double cx, cy, cz;
             bool vx, vy, vz;
-            h_entry(g, hc, e, j, k, cellplane, Fz, ry, rz, rx, cx, cy, cz, vx, vy, vz, fastdiv);
+            h_entry(g, hc, e, j, k, cellplane, Fz, ry, rz, rx, cx, cy, cz, vx, vy, vz, fastdiv,
+                    ax, ay, az);
             const int id = ids[gg - ia0];
             const bool magnetic = cellplane && j < ny && k < nz && s_mag[id];
             if (__builtin_expect(!magnetic, 1)) {
@@ -371,9 +382,9 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
                         q4 = xdiv(b4, g.d[0], rx); q5 = xdiv(b5, g.d[0], rx);
                     }
                     double cx = 0.0, cy = 0.0, cz = 0.0;   // em.py:217-231 order
-                    if (g.act[1]) { cx = cx + q0; cz = cz - q1; }
-                    if (g.act[2]) { cx = cx - q2; cy = cy + q3; }
-                    if (g.act[0]) { cy = cy - q4; cz = cz + q5; }
+                    if (ay) { cx = cx + q0; cz = cz - q1; }
+                    if (az) { cx = cx - q2; cy = cy + q3; }
+                    if (ax) { cy = cy - q4; cz = cz + q5; }
                     const int id = ids[f - ia0];
                     const double ca = s_cacb[2 * id], cb = s_cacb[2 * id + 1];
                     const double* Ex = hc.Ex;
@@ -388,8 +399,8 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
                     // entry (k=1 / k=nz-1) writes the tangential wall value; lines
                     // an x/y wall reads or writes are left to k_zfix (run after the
                     // x/y wall kernels, preserving the face order x0..z1)
-                    const bool zx = !(g.act[1] && (j <= 1 || j >= ny - 1));
-                    const bool zy = !(g.act[0] && (p <= 1 || p >= nx - 1));
+                    const bool zx = !(ay && (j <= 1 || j >= ny - 1));
+                    const bool zy = !(ax && (p <= 1 || p >= nx - 1));
                     bool wx = true, wy = true;
                     if ((zw0 && k == 0) || (zw1 && k == nz)) { wx = !zx; wy = !zy; }
                     if (wx) b.Eb[0][o] = w0;
@@ -405,7 +416,7 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
                         if (zx) b.Eb[0][o + 1] = z1pec ? 0.0 : exa + kk * (w0 - Ex[e + 1]);
                         if (zy) b.Eb[1][o + 1] = z1pec ? 0.0 : eya + kk * (w1 - Ey[e + 1]);
                     }
-                    const bool cp = p < nx || !g.act[0];
+                    const bool cp = p < nx || !ax;
                     if (j < ny && k < nz) b.Hb[0][o] = hx;
                     if (cp && k < nz) b.Hb[1][o] = hy;
                     if (cp && j < ny) b.Hb[2][o] = hz;
