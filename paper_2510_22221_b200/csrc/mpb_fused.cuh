@@ -8,6 +8,7 @@ namespace {
 struct FusedState {
     SweepCfg sc{};
     int V = 2;
+    int NT = kSweepThreads;
     bool F3 = true;
     int grid = 0;
     size_t smem = 0;
@@ -19,9 +20,9 @@ struct FusedState {
 
 FusedState* fused_of(mpb_handle* h) { return reinterpret_cast<FusedState*>(h->fused); }
 
-template <int V, bool F3>
+template <int V, bool F3, int NT = kSweepThreads>
 int set_smem_attr(size_t smem) {
-    CU(cudaFuncSetAttribute(k_sweep<V, F3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CU(cudaFuncSetAttribute(k_sweep<V, F3, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)smem));
     return MPB_OK;
 }
@@ -45,7 +46,13 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
     if (Fz == 1) sc.fz_magic = 0;   // j = f for Fz == 1 handled below
     // entries per CTA per plane: 2 per thread unless the plane is small
     fs->V = g.FyFz >= 8 * kSweepThreads * sms ? 4 : (g.FyFz >= 2 * kSweepThreads * 64 ? 2 : 1);
-    sc.T = fs->V * kSweepThreads;
+    // large 3D planes: 256-thread CTAs, two per SM (each one's barrier waits
+    // overlap the other's work); MPB_SWEEP_NT=512 selects one 512-thread CTA
+    fs->NT = kSweepThreads;
+    if (fs->V == 2 && g.act[0] && g.act[1] && g.act[2]) fs->NT = 256;
+    if (const char* e = getenv("MPB_SWEEP_NT"))
+        if (atoi(e) == 512) fs->NT = kSweepThreads;
+    sc.T = fs->V * fs->NT;
     if (const char* e = getenv("MPB_SWEEP_T")) {
         const int t = atoi(e);
         if (t > 0 && t <= sc.T) sc.T = t;
@@ -70,7 +77,7 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
                         fs->smem);
     // x-chunks: ~8 waves of one CTA per SM, chunks of >= 24 planes
     const int Fx = g.c1 - g.c0;                      // owned planes of this rank
-    int waves = 16;
+    int waves = fs->NT == 256 ? 32 : 16;
     if (const char* e = getenv("MPB_SWEEP_WAVES")) waves = std::max(1, atoi(e));
     const int want = std::max(1, (waves * sms + sc.tiles - 1) / sc.tiles);
     const int maxch = std::max(1, Fx / 24);
@@ -80,7 +87,9 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
     fs->grid = sc.tiles * sc.nchunks;
     fs->F3 = g.act[0] && g.act[1] && g.act[2];
     int rc;
-    if (fs->F3)
+    if (fs->NT == 256)
+        rc = set_smem_attr<2, true, 256>(fs->smem);
+    else if (fs->F3)
         rc = fs->V == 4 ? set_smem_attr<4, true>(fs->smem)
                         : (fs->V == 2 ? set_smem_attr<2, true>(fs->smem) : set_smem_attr<1, true>(fs->smem));
     else
@@ -172,7 +181,10 @@ int launch_fused(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s) {
 #define MPB_LAUNCH(VV, FF)                                                              \
     k_sweep<VV, FF><<<fs->grid, kSweepThreads, fs->smem, s>>>(g, b, h->mats, ids_view(h), \
                                                               h->st, fs->sc)
-    if (fs->F3) {
+    if (fs->NT == 256) {
+        k_sweep<2, true, 256><<<fs->grid, 256, fs->smem, s>>>(g, b, h->mats, ids_view(h), h->st,
+                                                             fs->sc);
+    } else if (fs->F3) {
         if (fs->V == 4) MPB_LAUNCH(4, true);
         else if (fs->V == 2) MPB_LAUNCH(2, true);
         else MPB_LAUNCH(1, true);

@@ -185,8 +185,8 @@ __device__ __forceinline__ void h_entry(const Geom& g, const HCtx& c, int e, int
     if (ax) { cy = cy - q4; cz = cz + q5; }
 }
 
-template <int V, bool F3>
-__global__ void __launch_bounds__(kSweepThreads, 1)
+template <int V, bool F3, int NT = kSweepThreads>
+__global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1)
 k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
         const uint8_t* __restrict__ gids, StepState* st, SweepCfg sc) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -306,7 +306,7 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
         const bool cellplane = p < nx || !ax;
 
         // ---- H^{n+1}(p, g) for g in [hlo, f1), in place --------------------
-        for (int gg = hlo + tid; gg < f1; gg += kSweepThreads) {
+        for (int gg = hlo + tid; gg < f1; gg += NT) {
             const int j = fz_div((uint32_t)gg, sc.fz_magic);
             const int k = gg - j * Fz;
             const int e = gg - a0;
@@ -346,7 +346,7 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
         const int64_t base = (int64_t)p * g.PP;
 #pragma unroll
         for (int v = 0; v < V; ++v) {
-            const int f = f0 + tid + v * kSweepThreads;
+            const int f = f0 + tid + v * NT;
             if (f < f1) {
                 const int e = f - a0;
                 const double hx = Hx[e], hy = Hy[e], hz = Hz[e];
