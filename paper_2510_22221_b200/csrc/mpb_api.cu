@@ -269,7 +269,7 @@ int phase_post(mpb_handle* h, int pa, cudaStream_t s, int64_t& launches,
         k_esweep<<<plane_grid, 256, 0, s>>>(g, b, h->mats, ids, h->st);
         ++launches;
     }
-    const int nface = h->variant == 1 ? 6 : 4;   // fused: z walls are in the sweep
+    const int nface = g.zin ? 4 : 6;   // fused: z walls are in the sweep
     for (int face = 0; face < nface; ++face) {
         if (!h->faces_active[face]) continue;
         const int axis = face >> 1;
@@ -279,7 +279,7 @@ int phase_post(mpb_handle* h, int pa, cudaStream_t s, int64_t& launches,
         k_wall<<<(unsigned)((cnt + 255) / 256), 256, 0, s>>>(g, b, h->mats, ids, h->st, face);
         ++launches;
     }
-    if (h->variant != 1) {
+    if (g.zin) {
         int rc = launch_zfix(h, g, b, s);
         if (rc) return rc;
         launches += zfix_launches(h);
@@ -419,8 +419,8 @@ int64_t launches_per_step(mpb_handle* h) {
     if (h->nranks == 1 && h->nmag > 0) n += 1;
     if (h->nranks > 1 && h->any_magnetic) n += 1 + (h->nmag > 0 ? 1 : 0);
     if (h->variant != 1 && h->nmag > 0) n += 1;
-    for (int f = 0; f < (h->variant == 1 ? 6 : 4); ++f) n += h->faces_active[f];
-    if (h->variant != 1) n += zfix_launches(h);
+    for (int f = 0; f < (h->g.zin ? 4 : 6); ++f) n += h->faces_active[f];
+    if (h->g.zin) n += zfix_launches(h);
     return n;
 }
 
@@ -599,6 +599,9 @@ int mpb_create(const mpb_setup* su, mpb_handle** out) {
     g.coef_h = su->coef_h;
     g.max_iters = su->llg_max_iters;
     g.tol = su->llg_tol;
+    g.zin = su->kernel_variant == 1 ? 0 : 1;
+    if (const char* e = getenv("MPB_ZWALL"))        // "kernel": separate z-wall launches
+        if (!strcmp(e, "kernel")) g.zin = 0;
     g.c0 = x_lo;
     g.c1 = x_hi == nx ? (int)F[0] : x_hi;
     h->lo = std::max(0, g.c0 - 1);

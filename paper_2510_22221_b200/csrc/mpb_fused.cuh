@@ -135,7 +135,7 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
                       cudaMemcpyHostToDevice));
     }
     // z-wall lines deferred to k_zfix (see mpb_sweep.cuh)
-    if (g.act[2] && (g.faces[4] != MPB_FACE_PMC || g.faces[5] != MPB_FACE_PMC)) {
+    if (g.zin && g.act[2] && (g.faces[4] != MPB_FACE_PMC || g.faces[5] != MPB_FACE_PMC)) {
         std::set<int> jset, iset;
         if (g.act[1]) for (int j : {0, 1, g.n[1] - 1, g.n[1]}) jset.insert(j);
         if (g.act[0])

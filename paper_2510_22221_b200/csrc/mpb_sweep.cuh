@@ -275,8 +275,8 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
     const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
     // collapsed axes: their (unused) quotients must not trip the guard
     const bool fastdiv = sc.fastdiv != 0 && ax && ay && az;
-    const bool zw0 = az && g.faces[4] != MPB_FACE_PMC;
-    const bool zw1 = az && g.faces[5] != MPB_FACE_PMC;
+    const bool zw0 = g.zin && az && g.faces[4] != MPB_FACE_PMC;
+    const bool zw1 = g.zin && az && g.faces[5] != MPB_FACE_PMC;
     const bool z0pec = g.faces[4] == MPB_FACE_PEC, z1pec = g.faces[5] == MPB_FACE_PEC;
     const bool pmc_x0 = g.faces[0] == MPB_FACE_PMC, pmc_x1 = g.faces[1] == MPB_FACE_PMC;
     const bool pmc_y0 = g.faces[2] == MPB_FACE_PMC, pmc_y1 = g.faces[3] == MPB_FACE_PMC;
@@ -467,7 +467,8 @@ __global__ void __launch_bounds__(256) k_edefer(Geom g, Bufs b,
     const E3 w = e_plain_at(g, b, mats, ids, i, j, k, o);
     const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
     const bool az = g.act[2];
-    const bool zw0 = az && g.faces[4] != MPB_FACE_PMC, zw1 = az && g.faces[5] != MPB_FACE_PMC;
+    const bool zw0 = g.zin && az && g.faces[4] != MPB_FACE_PMC;
+    const bool zw1 = g.zin && az && g.faces[5] != MPB_FACE_PMC;
     const bool z0pec = g.faces[4] == MPB_FACE_PEC, z1pec = g.faces[5] == MPB_FACE_PEC;
     const bool zx = !(g.act[1] && (j <= 1 || j >= ny - 1));
     const bool zy = !(g.act[0] && (i <= 1 || i >= nx - 1));
