@@ -70,6 +70,7 @@ typedef struct mpb_material {
     double hbias[3];
     int32_t magnetic;       /* Ms > 0 */
     int32_t pad_;
+    double eps;             /* eps0*eps_r      em.py:377 (energy diagnostic)  */
 } mpb_material;
 
 typedef struct mpb_setup {
@@ -194,6 +195,13 @@ MPB_API int64_t mpb_launch_count(mpb_handle* h);
  * and the compiler's IEEE x/d) and counts bitwise mismatches. */
 MPB_API int mpb_selftest_division(int32_t device, double d, const double* x, int64_t n,
                                   int64_t* mismatches, double* first_bad);
+
+/* Discrete field energy of the current device state (reference
+ * em.total_energy, em.py:366-383): (1/2 sum eps E^2 + 1/2 mu0 sum H^2
+ * - mu0 sum M.Hbias) dV over this rank's owned planes (multi-rank: sum the
+ * ranks).  Deterministic fixed-order reduction; equal to the reference to
+ * rounding (summation order differs), not bitwise. */
+MPB_API int mpb_total_energy(mpb_handle* h, double* out);
 
 /* Device bytes held by the handle. */
 MPB_API int64_t mpb_device_bytes(mpb_handle* h);

@@ -1036,6 +1036,49 @@ int mpb_group_run(mpb_handle* const* hs, int32_t n, int64_t n0, int64_t nsteps,
     return rc;
 }
 
+int mpb_total_energy(mpb_handle* h, double* out) {
+    g_err.clear();
+    if (!h || !out) return fail_msg(MPB_EINVAL, "null argument");
+    CU(cudaSetDevice(h->device));
+    CU(cudaStreamSynchronize(h->stream));
+    const Geom& g = h->g;
+    const int p = h->parity;
+    const double* E[3];
+    const double* Hh[3];
+    const double* Mm[3];
+    for (int c = 0; c < 3; ++c) {
+        E[c] = view(h->E[p][c], h);
+        Hh[c] = view(h->H[p][c], h);
+        Mm[c] = h->M[p][c];
+    }
+    const double** dptr = nullptr;
+    CU(cudaMalloc(&dptr, 9 * sizeof(double*)));
+    const double* hp[9] = {E[0], E[1], E[2], Hh[0], Hh[1], Hh[2], Mm[0], Mm[1], Mm[2]};
+    CU(cudaMemcpy(dptr, hp, sizeof hp, cudaMemcpyHostToDevice));
+    const int blocks = 1184;
+    double* partial = nullptr;
+    CU(cudaMalloc(&partial, 3 * blocks * sizeof(double)));
+    k_energy_partial<<<blocks, 256, 0, h->stream>>>(g, dptr, dptr + 3, dptr + 6, h->mats,
+                                                    ids_view(h), partial);
+    CU(cudaGetLastError());
+    std::vector<double> hpart((size_t)3 * blocks);
+    CU(cudaMemcpyAsync(hpart.data(), partial, hpart.size() * sizeof(double),
+                       cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    cudaFree(partial);
+    cudaFree(dptr);
+    double se = 0.0, sh = 0.0, sm = 0.0;
+    for (int b = 0; b < blocks; ++b) {
+        se += hpart[3 * b];
+        sh += hpart[3 * b + 1];
+        sm += hpart[3 * b + 2];
+    }
+    const double mu0 = 4e-7 * 3.141592653589793;
+    const double vol = g.d[0] * g.d[1] * g.d[2];
+    *out = (0.5 * se + 0.5 * mu0 * sh + (-mu0) * sm) * vol;
+    return MPB_OK;
+}
+
 int64_t mpb_launch_count(mpb_handle* h) { return h ? h->launches_last : 0; }
 
 int64_t mpb_device_bytes(mpb_handle* h) { return h ? h->bytes : 0; }

@@ -428,6 +428,46 @@ __global__ void __launch_bounds__(256) k_wall(Geom g, Bufs b,
 }
 
 // ---------------------------------------------------------------------------
+// Energy diagnostic (em.py:366-383): per-block partial sums in a fixed
+// order, then one block combines them -- deterministic run to run.
+// out[0..2] per block: sum eps E^2, sum H^2, sum M.Hbias.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_energy_partial(Geom g, const double* const* E,
+                                                        const double* const* H,
+                                                        const double* const* M,
+                                                        const mpb_material* __restrict__ mats,
+                                                        const uint8_t* __restrict__ ids,
+                                                        double* partial) {
+    __shared__ double red[3][256];
+    const int64_t nent = (int64_t)(g.c1 - g.c0) * g.FyFz;
+    double se = 0.0, sh = 0.0, sm = 0.0;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nent;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const int i = g.c0 + (int)(q / g.FyFz);
+        const int f = (int)(q - (int64_t)(i - g.c0) * g.FyFz);
+        const int64_t o = i * g.PP + f;
+        const mpb_material& m = mats[ids[o]];
+        se += m.eps * (E[0][o] * E[0][o]) + m.eps * (E[1][o] * E[1][o]) +
+              m.eps * (E[2][o] * E[2][o]);
+        sh += H[0][o] * H[0][o] + H[1][o] * H[1][o] + H[2][o] * H[2][o];
+        const int j = f / g.F[2], k = f - j * g.F[2];
+        if (M[0] && i >= g.mx0 && i < g.mx1 && i < g.n[0] && j < g.n[1] && k < g.n[2]) {
+            const int64_t om = (int64_t)(i - g.mx0) * g.PP + f;
+            sm += M[0][om] * m.hbias[0] + M[1][om] * m.hbias[1] + M[2][om] * m.hbias[2];
+        }
+    }
+    red[0][threadIdx.x] = se; red[1][threadIdx.x] = sh; red[2][threadIdx.x] = sm;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w)
+            for (int c = 0; c < 3; ++c) red[c][threadIdx.x] += red[c][threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)
+        for (int c = 0; c < 3; ++c) partial[3 * blockIdx.x + c] = red[c][0];
+}
+
+// ---------------------------------------------------------------------------
 // End of step: soft source (em.py:276-282), probes (sim.py:170-171), r*
 // record (sim.py:167), reset of the LLG bookkeeping for the next step.
 // One block.

@@ -110,6 +110,7 @@ def material_table(materials, dt: float, spacings):
         for c in range(3):
             m.hbias[c] = hb[c][q]
         m.magnetic = int(bool(ismag[q]))
+        m.eps = eps[q]
     return ids, table
 
 
@@ -245,6 +246,12 @@ class DeviceRun:
         N.check(self.lib.mpb_kernel_time(self.h, C.byref(ms), C.byref(cnt),
                                          C.byref(name)))
         return ms.value, cnt.value, name.value.decode()
+
+    def total_energy(self) -> float:
+        """em.total_energy of the current device state (this rank's planes)."""
+        out = C.c_double()
+        N.check(self.lib.mpb_total_energy(self.h, C.byref(out)))
+        return out.value
 
     def launch_count(self) -> int:
         return int(self.lib.mpb_launch_count(self.h))

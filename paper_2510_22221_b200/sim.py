@@ -233,3 +233,54 @@ def load_snapshot(path) -> dict:
             probes[(comp, (int(i), int(j), int(k)))] = data[key]
     return {"fields": fields, "step": int(data["step"]), "probes": probes,
             "iterations": data["iterations"]}
+
+
+# ---------------------------------------------------------------------------
+# bias sweep (sim.py:227-260): one run per bias, replicas across GPUs
+# ---------------------------------------------------------------------------
+
+@dataclass
+class SpectrumMap:
+    biases: np.ndarray
+    freqs: np.ndarray
+    mags: np.ndarray
+
+
+def _sweep_one(args):
+    config, bias, device = args
+    from .analysis import fft_magnitude
+    res = run(config, bias=bias, device=device)
+    probe = list(res.probes.values())[config.spectrum_probe]
+    spec = fft_magnitude(probe, window="hann")
+    return spec.freqs, spec.mags
+
+
+def _gpu_count() -> int:
+    try:
+        import torch
+        return torch.cuda.device_count()
+    except Exception:
+        return 0
+
+
+def sweep(config: SimConfig, biases=None, parallel: int = 1) -> SpectrumMap:
+    """Hann-window FFT magnitude of the spectrum probe for every bias.
+
+    ``parallel > 1`` runs up to ``parallel`` biases at once, one process per
+    GPU (spawned, never forked after CUDA init).  Rows are assembled in bias
+    order, so serial and parallel sweeps are identical (reference
+    sim.py:243-260).
+    """
+    biases = np.asarray(config.bias_sweep if biases is None else biases, float)
+    if biases.size == 0:
+        raise ValueError("bias sweep must be non-empty")
+    ngpu = max(1, _gpu_count())
+    workers = max(1, min(parallel, ngpu, biases.size))
+    jobs = [(config, float(b), i % workers) for i, b in enumerate(biases)]
+    if workers > 1:
+        import multiprocessing as mp
+        with mp.get_context("spawn").Pool(workers) as pool:
+            rows = pool.map(_sweep_one, jobs)
+    else:
+        rows = [_sweep_one(j) for j in jobs]
+    return SpectrumMap(biases=biases, freqs=rows[0][0], mags=np.stack([r[1] for r in rows]))

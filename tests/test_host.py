@@ -29,7 +29,7 @@ def test_library_exports_every_header_symbol():
 
 def test_struct_layout_matches_header():
     # offsets the C side relies on (x86-64 SysV)
-    assert C.sizeof(_native.Material) == 11 * 8 + 8
+    assert C.sizeof(_native.Material) == 11 * 8 + 8 + 8
     assert _native.Setup.dt.offset == 40
 
 
