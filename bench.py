@@ -55,6 +55,11 @@ def _bytes_per_cell(f_mag: float) -> float:
     return 96.0 + 48.0 * f_mag
 
 
+# The dominant kernel (k_sweep) moves the six field components; M is read and
+# written by k_llg_local, so the sweep's algorithmic bytes are 96 B/cell.
+SWEEP_BYTES_PER_CELL = 96.0
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons, timestamped; summary() keeps the
     samples that fall inside [t0, t1] (the timed region)."""
@@ -331,9 +336,10 @@ def main() -> None:
         t_e2e = float(t.item())
     e2e = cells * world * e2e_steps / t_e2e / 1e9
     peak, peak_kind = _peaks()
-    bpc = _bytes_per_cell(f_mag)
+    bpc = SWEEP_BYTES_PER_CELL if kname == "k_sweep" else _bytes_per_cell(f_mag)
     per_launch_ms = kms / max(1, klaunch)
     achieved = cells * bpc / (per_launch_ms * 1e-3) / 1e9 if klaunch else None
+    step_frac = value / world * _bytes_per_cell(f_mag) / peak
     traffic = None
     tp = ROOT / "profiles" / "traffic.json"
     if tp.exists():
@@ -370,7 +376,9 @@ def main() -> None:
                      "traffic": traffic, "kernel": kname,
                      "bytes_per_cell": bpc, "peak_kind": peak_kind,
                      "kernel_ms_per_step": per_launch_ms,
-                     "kernel_share_of_step": per_launch_ms / (ms / args.steps)},
+                     "kernel_share_of_step": per_launch_ms / (ms / args.steps),
+                     "whole_step_frac": step_frac,
+                     "whole_step_bytes_per_cell": _bytes_per_cell(f_mag)},
         "cpu_baseline": cpu,
         "clocks": clk.summary(t_wall0, t_wall1),
         "gpu_launches": launches,

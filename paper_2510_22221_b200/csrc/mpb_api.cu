@@ -118,6 +118,7 @@ int launch_fused(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s);
 int launch_deferred(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s);
 int launch_zfix(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s);
 int zfix_launches(mpb_handle* h);
+int launch_llg_local(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s);
 const char* fused_kernel_name();
 }  // namespace
 
@@ -212,6 +213,10 @@ int phase_sweep(mpb_handle* h, int pa, cudaStream_t s, int64_t& launches) {
     } else {
         int rc = launch_fused(h, g, b, s);
         if (rc) return rc;
+        if (h->nmag > 0) {
+            if ((rc = launch_llg_local(h, g, b, s))) return rc;
+            ++launches;
+        }
     }
     ++launches;
     return MPB_OK;
@@ -418,7 +423,7 @@ int64_t launches_per_step(mpb_handle* h) {
     int64_t n = (h->variant == 1 ? 2 : 1) + 1;
     if (h->nranks == 1 && h->nmag > 0) n += 1;
     if (h->nranks > 1 && h->any_magnetic) n += 1 + (h->nmag > 0 ? 1 : 0);
-    if (h->variant != 1 && h->nmag > 0) n += 1;
+    if (h->variant != 1 && h->nmag > 0) n += 2;   // k_llg_local + k_edefer
     for (int f = 0; f < (h->g.zin ? 4 : 6); ++f) n += h->faces_active[f];
     if (h->g.zin) n += zfix_launches(h);
     return n;

@@ -167,6 +167,16 @@ int launch_zfix(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s) {
 
 int zfix_launches(mpb_handle* h) { return fused_of(h)->nzlines ? 1 : 0; }
 
+// LLG of the magnetic cells after the pure-Maxwell sweep (fused variant).
+int launch_llg_local(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s) {
+    if (!h->nmag) return MPB_OK;
+    const size_t smem = (size_t)(g.max_iters + 2) * sizeof(unsigned long long);
+    k_llg_local<<<(h->nmag + 255) / 256, 256, smem, s>>>(g, b, h->mats, ids_view(h),
+                                                        h->magcells, h->magowned, h->nmag,
+                                                        h->st);
+    return MPB_OK;
+}
+
 void destroy_fused(mpb_handle* h) {
     FusedState* fs = fused_of(h);
     if (!fs) return;
@@ -201,7 +211,7 @@ int launch_deferred(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s)
     FusedState* fs = fused_of(h);
     if (!fs->ndefer) return MPB_OK;
     k_edefer<<<(fs->ndefer + 255) / 256, 256, 0, s>>>(g, b, h->mats, ids_view(h), fs->defer,
-                                                    fs->ndefer, h->st);
+                                                    fs->ndefer, h->st, 1);
     return MPB_OK;
 }
 

@@ -191,12 +191,10 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
         const uint8_t* __restrict__ gids, StepState* st, SweepCfg sc) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ uint64_t bars[kSlots];
-    __shared__ int s_rc[2];
-    __shared__ int s_anymag;
+
     __shared__ double s_cacb[MPB_MAX_MATERIALS * 2];
-    __shared__ unsigned char s_mag[MPB_MAX_MATERIALS];
+
     __shared__ double s_murz[MPB_MAX_MATERIALS];
-    unsigned long long* s_hist = reinterpret_cast<unsigned long long*>(smem);
     unsigned char* ring = smem + sc.ring_offset;
 
     if (st->fail) return;
@@ -229,12 +227,9 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
     for (int q = tid; q < sc.nmat; q += blockDim.x) {
         s_cacb[2 * q] = mats[q].ca;
         s_cacb[2 * q + 1] = mats[q].cb;
-        s_mag[q] = (unsigned char)mats[q].magnetic;
         s_murz[q] = mats[q].mur_k[2];
     }
-    for (int r = tid; r <= g.max_iters + 1; r += blockDim.x) s_hist[r] = 0ull;
     if (tid == 0) {
-        s_rc[0] = 0x7fffffff; s_rc[1] = 0; s_anymag = 0;
         for (int q = 0; q < kSlots; ++q) mbar_init(&bars[q], 1);
         mbar_fence_init();
     }
@@ -314,28 +309,11 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
             bool vx, vy, vz;
             h_entry(g, hc, e, j, k, cellplane, Fz, ry, rz, rx, cx, cy, cz, vx, vy, vz, fastdiv,
                     ax, ay, az);
-            const int id = ids[gg - ia0];
-            const bool magnetic = cellplane && j < ny && k < nz && s_mag[id];
-            if (__builtin_expect(!magnetic, 1)) {
-                if (vx) hc.Hx[e] = hc.Hx[e] - g.coef_h * cx;
-                if (vy) hc.Hy[e] = hc.Hy[e] - g.coef_h * cy;
-                if (vz) hc.Hz[e] = hc.Hz[e] - g.coef_h * cz;
-            } else {
-                const int64_t om = (int64_t)(p - g.mx0) * g.PP + gg;
-                const double hn[3] = {hc.Hx[e], hc.Hy[e], hc.Hz[e]};
-                const double mn[3] = {b.Ma[0][om], b.Ma[1][om], b.Ma[2][om]};
-                const double ce[3] = {cx, cy, cz};
-                double ho[3], mo[3];
-                const bool own = emit && gg >= f0;
-                const int rc = llg_cell_local(mats, id, &g, hn, mn, ce, ho, mo, s_hist, own);
-                hc.Hx[e] = ho[0]; hc.Hy[e] = ho[1]; hc.Hz[e] = ho[2];
-                if (own) {
-                    b.Mb[0][om] = mo[0]; b.Mb[1][om] = mo[1]; b.Mb[2][om] = mo[2];
-                    atomicMin(&s_rc[0], rc);
-                    atomicMax(&s_rc[1], rc);
-                    s_anymag = 1;
-                }
-            }
+            // magnetic cells get the plain update here too; k_llg_local
+            // replaces their H (and the E entries around them, k_edefer)
+            if (vx) hc.Hx[e] = hc.Hx[e] - g.coef_h * cx;
+            if (vy) hc.Hy[e] = hc.Hy[e] - g.coef_h * cy;
+            if (vz) hc.Hz[e] = hc.Hz[e] - g.coef_h * cz;
         }
         __syncthreads();
 
@@ -436,17 +414,53 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
             }
         }
     }
+}
+
+// LLG of the magnetic cells after the (pure Maxwell) sweep: each cell runs
+// its fixed point to its local stop from the untouched step-n state (E^n for
+// curl E, H^n, M^n) and writes H^{n+1}, M^{n+1}; per-block residual history and
+// local-stop range feed the global stop rule (k_llg_fixup / all-reduce).
+// Ghost-plane copies (slabs) are computed for their H only.
+__global__ void __launch_bounds__(256) k_llg_local(Geom g, Bufs b,
+                                                   const mpb_material* __restrict__ mats,
+                                                   const uint8_t* __restrict__ ids,
+                                                   const int2* __restrict__ cells,
+                                                   const unsigned char* __restrict__ owned,
+                                                   int ncells, StepState* st) {
+    extern __shared__ unsigned long long lhist[];
+    __shared__ int lrc[2];
+    if (st->fail) return;
+    CtaLlgStats cs{lhist, lrc};
+    cta_stats_init(cs, g.max_iters);
     __syncthreads();
-    if (s_anymag) {
-        for (int r = 1 + tid; r <= g.max_iters; r += blockDim.x) {
-            const unsigned long long v = s_hist[r];
-            if (v) atomicMax(&st->hist[r], v);
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q < ncells) {
+        const int i = cells[q].x, f = cells[q].y;
+        const int64_t o = i * g.PP + f;
+        const int64_t om = (int64_t)(i - g.mx0) * g.PP + f;
+        LlgCell s;
+        const Curl3 c = curl_e_at(g, b.Ea, o, g.PP, g.F[2], true, true, true);
+        for (int k = 0; k < 3; ++k) { s.Hn[k] = b.Ha[k][o]; s.Mn[k] = b.Ma[k][om]; }
+        s.cE[0] = c.x; s.cE[1] = c.y; s.cE[2] = c.z;
+        llg_setup(s, mats[ids[o]]);
+        const bool own = owned[q] != 0;
+        double Hr[3] = {s.Hn[0], s.Hn[1], s.Hn[2]};
+        double Mr[3] = {s.Mn[0], s.Mn[1], s.Mn[2]};
+        int rc = g.max_iters + 1;
+        for (int r = 1; r <= g.max_iters; ++r) {
+            const double res = llg_iterate(s, g.coef_h, Hr, Mr);
+            if (own) atomicMax(&cs.hist[r], dbits(res));
+            if (res <= g.tol) { rc = r; break; }
         }
-        if (tid == 0) {
-            atomicMax(&st->rc_negmin, -s_rc[0]);
-            atomicMax(&st->rc_max, s_rc[1]);
+        for (int k = 0; k < 3; ++k) b.Hb[k][o] = Hr[k];
+        if (own) {
+            for (int k = 0; k < 3; ++k) b.Mb[k][om] = Mr[k];
+            atomicMin(&cs.rc[0], rc);
+            atomicMax(&cs.rc[1], rc);
         }
     }
+    __syncthreads();
+    if (lrc[1] > 0) cta_stats_flush(cs, g.max_iters, st);
 }
 
 // E entries whose curl-H stencil touches a magnetic H entry, recomputed after
@@ -456,8 +470,8 @@ __global__ void __launch_bounds__(256) k_edefer(Geom g, Bufs b,
                                                 const mpb_material* __restrict__ mats,
                                                 const uint8_t* __restrict__ ids,
                                                 const int2* __restrict__ list, int n,
-                                                const StepState* st) {
-    if (st->fail || !st->fixup_ran) return;
+                                                const StepState* st, int always) {
+    if (st->fail || (!always && !st->fixup_ran)) return;
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= n) return;
     const int i = list[q].x, f = list[q].y;
