@@ -115,29 +115,6 @@ __global__ void k_div_selftest(const double* __restrict__ x, int64_t n, double d
     }
 }
 
-// LLG for one cell, kept out of line so the rare path does not inflate the
-// register allocation of the streaming path.
-__device__ __noinline__ int llg_cell_local(const mpb_material* __restrict__ mats, int id,
-                                          const Geom* gp, const double* hn,
-                                          const double* mn, const double* ce, double* hout,
-                                          double* mout, unsigned long long* shist,
-                                          int record) {
-    const Geom& g = *gp;
-    LlgCell s;
-    for (int c = 0; c < 3; ++c) { s.Hn[c] = hn[c]; s.Mn[c] = mn[c]; s.cE[c] = ce[c]; }
-    llg_setup(s, mats[id]);
-    double Hr[3] = {s.Hn[0], s.Hn[1], s.Hn[2]};
-    double Mr[3] = {s.Mn[0], s.Mn[1], s.Mn[2]};
-    int rc = g.max_iters + 1;
-    for (int r = 1; r <= g.max_iters; ++r) {
-        const double res = llg_iterate(s, g.coef_h, Hr, Mr);
-        if (record) atomicMax(&shist[r], dbits(res));
-        if (res <= g.tol) { rc = r; break; }
-    }
-    for (int c = 0; c < 3; ++c) { hout[c] = Hr[c]; mout[c] = Mr[c]; }
-    return rc;
-}
-
 // H^{n+1} at one entry of the staged plane (in place in shared memory).
 // Straight-line: all six differences and divisions are issued back to back
 // and the division guard is checked once for the batch.
