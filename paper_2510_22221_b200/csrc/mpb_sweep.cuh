@@ -262,15 +262,10 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
         const int s = slot(p);
         const bool xnext = ax && p < nx;                 // plane p+1 used by dx terms
         const int s1 = slot(p + 1);
-        if (tid == 0) {
-            mbar_wait(&bars[s], ((p - pstart) / kSlots) & 1);
-            if (xnext) mbar_wait(&bars[s1], ((p + 1 - pstart) / kSlots) & 1);
-        }
-        __syncthreads();   // staged data visible; E phase of p-1 done everywhere
-        if (tid == 0 && p > pstart && p + 2 <= plast) {
-            fence_proxy_async();
-            issue(p + 2);  // into the slot plane p-1 just released
-        }
+        // every thread waits for the staged planes itself (no CTA barrier
+        // here): the only barrier per plane is the one between the phases
+        mbar_wait(&bars[s], ((p - pstart) / kSlots) & 1);
+        if (xnext) mbar_wait(&bars[s1], ((p + 1 - pstart) / kSlots) & 1);
         HCtx hc{sE(s, 0), sE(s, 1), sE(s, 2), sE(s1, 1), sE(s1, 2),
                 sH(s, 0), sH(s, 1), sH(s, 2)};
         const unsigned char* ids = sI(s);
@@ -292,7 +287,13 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
             if (vy) hc.Hy[e] = hc.Hy[e] - g.coef_h * cy;
             if (vz) hc.Hz[e] = hc.Hz[e] - g.coef_h * cz;
         }
+        // H^{n+1}(p) complete everywhere, and every thread is past E(p-1) and
+        // H(p), the last readers of plane p-1's slot: refill it with p+2
         __syncthreads();
+        if (tid == 0 && p > pstart && p + 2 <= plast) {
+            fence_proxy_async();
+            issue(p + 2);
+        }
 
         // ---- E^{n+1}(p, f) for the owned range ------------------------------
         const double* Hx = hc.Hx;
