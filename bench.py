@@ -324,6 +324,14 @@ def main() -> None:
     value = cells * world * args.steps / (ms * 1e-3) / 1e9
     # end-to-end through the C ABI with host buffers (mpb_run)
     e2e_steps = args.e2e_steps or args.steps
+    # untimed warm-up of the host-buffer path: allocates its staging buffers
+    # and instantiates the CUDA graph (the timed run above used per-kernel
+    # events, which disable graphs)
+    warm = 32
+    _, _, fail = dev.run(total, sim.source_values(cfg.source, cfg.dt, total, total + warm))
+    if fail is not None:
+        raise RuntimeError(f"LLG failure in e2e warm-up: {fail}")
+    total += warm
     host_src = sim.source_values(cfg.source, cfg.dt, total, total + e2e_steps)
     barrier()
     torch.cuda.synchronize()
