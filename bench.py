@@ -8,6 +8,8 @@ Workload: C4 of SURVEY 8d -- 1024x1024x128 cells per GPU (CPW line on a Si
 substrate + YIG film, all-MUR1 walls, fp64), the per-GPU configuration the
 weak-scaling metric is quoted on.  A "step" is one full coupled step
 (curl E, H + LLG fixed point, curl H, E, walls, source, probes) of that grid.
+`--config c5 [--scaling strong]`: the fixed 2048x2048x256 grid (BASELINE
+configs[4]) split over the N GPUs (110 GB of device state on one B200).
 
 Prints ONE JSON line on rank 0:
   value  -- Gcell-updates/s over all ranks, state resident in HBM, device
@@ -137,15 +139,20 @@ def synthetic_state(fs, kind: str):
     out = {}
     for q, n in enumerate(("Ex", "Ey", "Ez", "Hx", "Hy", "Hz")):
         scale = 1e3 * (1.0 + 0.1 * q) if n[0] == "E" else 2.65 * (1.0 + 0.1 * q)
-        out[n] = np.roll(base, q, axis=-1) * scale
+        out[n] = np.roll(base, q, axis=-1)
+        out[n] *= scale                      # in place: C5 fields are 8.6 GB each
     return out
 
 
-def weak_scaled_slab(cfg, keys, world, rank, local, args):
-    """Weak scaling (SURVEY 8e / BASELINE C4): the global grid is the C4
-    geometry repeated along x, (nx * world) x ny x nz; rank r owns the x-slab
-    [nx r, nx (r+1)) and exchanges boundary planes with its neighbours over
-    NCCL every step.  Source and probes live on rank 0's slab."""
+def slab_run(cfg, keys, world, rank, local, args):
+    """One rank's x-slab, NCCL exchange with its neighbours.
+
+    weak (C4, BASELINE configs[3]): the global grid is the config's geometry
+    repeated along x, (nx * world) x ny x nz; rank r owns [nx r, nx (r+1));
+    source on rank 0's slab, no probes.
+    strong (C5, configs[4]): the config's own grid split into `world` slabs;
+    source and probes where the config puts them.
+    Materials stay painted (lazy): each rank builds only its slab's ids."""
     import torch.distributed as dist
     from dataclasses import replace
 
@@ -155,21 +162,18 @@ def weak_scaled_slab(cfg, keys, world, rank, local, args):
     from paper_2510_22221_b200.sim import _device_run_args
 
     g = cfg.grid
-    ggrid = GridSpec(g.nx * world, g.ny, g.nz, g.dx, g.dy, g.dz)
-    gcfg = replace(cfg, grid=ggrid, probes=())
-    nccl_id = parallel.nccl_unique_id(dist)
-    slab = replace(parallel.make_slabs(ggrid.nx, world, True)[rank], nccl_id=nccl_id)
+    nccl_id = parallel.nccl_unique_id(dist) if world > 1 else bytes(128)
+    if args.scaling == "weak":
+        ggrid = GridSpec(g.nx * world, g.ny, g.nz, g.dx, g.dy, g.dz)
+        gcfg = replace(cfg, grid=ggrid, probes=())
+        keys = []
+    else:
+        ggrid, gcfg = g, cfg
+    any_mag = cfg.materials.magnetic_count() > 0
+    slab = replace(parallel.make_slabs(ggrid.nx, world, any_mag)[rank], nccl_id=nccl_id)
     c0, c1 = slab.cell_range
-    period = np.arange(c0, c1) % g.nx          # C4 repeated along x
-
-    class Slab:
-        pass
-    mats = Slab()
-    for name in ("sigma", "eps_r", "Ms", "alpha", "gamma_e"):
-        setattr(mats, name, np.ascontiguousarray(np.asarray(getattr(cfg.materials, name))[period]))
-    mats.Hbias = np.ascontiguousarray(np.asarray(cfg.materials.Hbias)[:, period])
-    mats.shape = mats.Ms.shape
-    mats.magnetic_mask = mats.Ms > 0.0
+    mats = (cfg.materials.tiled_region(c0, c1) if args.scaling == "weak"
+            else cfg.materials.region(c0, c1))
     a = _device_run_args(gcfg, keys)
     dev = DeviceRun(ggrid, mats, a["boundaries"], a["source_loc"], a["source_pol"], keys,
                     cfg.llg_params, cfg.dt, device=local, kernel_variant=args.variant,
@@ -177,7 +181,8 @@ def weak_scaled_slab(cfg, keys, world, rank, local, args):
     f0, f1 = slab.field_range
     st = synthetic_state((f1 - f0,) + tuple(ggrid.field_shape[1:]), args.init)
     dev.load_state(st, initial_magnetization(mats))
-    return dev
+    del st
+    return dev, (slab.x_hi - slab.x_lo) * g.ny * g.nz
 
 
 def cpu_oracle_sample(cfg_name: str, steps: int):
@@ -303,7 +308,11 @@ def main() -> None:
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=0)
     ap.add_argument("--init", default="random", choices=["random", "zero"])
+    ap.add_argument("--scaling", default=None, choices=["weak", "strong"],
+                    help="multi-GPU mode (default: weak for c1-c4, strong for c5)")
     args = ap.parse_args()
+    if args.scaling is None:
+        args.scaling = "strong" if args.config == "c5" else "weak"
     if args.impl == "reference":
         run_reference(args)
         return
@@ -321,9 +330,10 @@ def main() -> None:
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    cfg = load_config(ROOT / CONFIGS[args.config])
-    cells = int(np.prod(cfg.grid.cell_shape))
-    mag = int(np.count_nonzero(cfg.materials.Ms > 0))
+    # painted (lazy) materials: no dense per-cell host maps (C5 would need 69 GB)
+    cfg = load_config(ROOT / CONFIGS[args.config], lazy=True)
+    cells = int(np.prod(cfg.grid.cell_shape))        # per GPU (weak) / total (strong)
+    mag = cfg.materials.magnetic_count()
     f_mag = mag / cells
     keys = [(p[0], (p[1], p[2], p[3])) for p in cfg.probes]
     keys = list(dict.fromkeys(keys))
@@ -332,8 +342,10 @@ def main() -> None:
                               kernel_variant=args.variant)
         dev.load_state(synthetic_state(cfg.grid.field_shape, args.init),
                        initial_magnetization(cfg.materials))
+        rank_cells = cells
     else:
-        dev = weak_scaled_slab(cfg, keys, world, rank, local, args)
+        dev, rank_cells = slab_run(cfg, keys, world, rank, local, args)
+    total_cells = cells * world if args.scaling == "weak" else cells
     total = args.warmup + args.steps
     src = torch.tensor(sim.source_values(cfg.source, cfg.dt, 0, total),
                        dtype=torch.float64, device="cuda")
@@ -380,7 +392,7 @@ def main() -> None:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
-    value = cells * world * args.steps / (ms * 1e-3) / 1e9
+    value = total_cells * args.steps / (ms * 1e-3) / 1e9
     # end-to-end through the C ABI with host buffers (mpb_run)
     e2e_steps = args.e2e_steps or args.steps
     # untimed warm-up of the host-buffer path: allocates its staging buffers
@@ -401,15 +413,15 @@ def main() -> None:
         t = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         t_e2e = float(t.item())
-    e2e = cells * world * e2e_steps / t_e2e / 1e9
+    e2e = total_cells * e2e_steps / t_e2e / 1e9
     peak, peak_kind = _peaks()
     bpc = SWEEP_BYTES_PER_CELL if kname == "k_sweep" else _bytes_per_cell(f_mag)
     per_launch_ms = kms / max(1, klaunch)
-    achieved = cells * bpc / (per_launch_ms * 1e-3) / 1e9 if klaunch else None
-    step_frac = value / world * _bytes_per_cell(f_mag) / peak
+    achieved = rank_cells * bpc / (per_launch_ms * 1e-3) / 1e9 if klaunch else None
+    step_frac = value / world * _bytes_per_cell(f_mag) / peak   # per-GPU average
     traffic = None
     tp = ROOT / "profiles" / "traffic.json"
-    if tp.exists():
+    if tp.exists() and args.config == "c4" and world == 1:   # captured on C4, 1 GPU
         traffic = json.loads(tp.read_text()).get(kname)
     if rank != 0:
         dev.close()
@@ -425,11 +437,14 @@ def main() -> None:
         "metric": METRIC, "value": value, "unit": "Gcell-updates/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": f"{args.config.upper()} {'x'.join(map(str, cfg.grid.cell_shape))} "
-                               f"cells per GPU, CPW + YIG film, all-MUR1, fp64",
-                   "config_file": CONFIGS[args.config], "cells_per_gpu": cells,
+                               + ("cells per GPU" if args.scaling == "weak" else
+                                  f"cells split over {world} GPU(s)")
+                               + ", CPW + YIG film, all-MUR1, fp64",
+                   "config_file": CONFIGS[args.config], "cells_per_gpu": rank_cells,
+                   "cells_total": total_cells,
                    "magnetic_fraction": f_mag,
                    "parallelism": f"x-slab x{world}" if world > 1 else "single GPU",
                    "l2": "state (2 x 6 fp64 fields) >> 126 MB L2; no flush needed",

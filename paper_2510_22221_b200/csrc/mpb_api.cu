@@ -26,6 +26,12 @@ namespace {
 
 thread_local std::string g_err;
 
+inline uint64_t dbits_host(double x) {
+    uint64_t u;
+    memcpy(&u, &x, sizeof u);
+    return u;
+}
+
 int fail_msg(int code, const char* fmt, ...) {
     char buf[1024];
     va_list ap;
@@ -99,6 +105,9 @@ struct mpb_handle {
     cudaGraphExec_t graph[2] = {nullptr, nullptr};
     // host copy of M on the local cell planes (cells outside the device M
     // range never change)
+    // M of the cell planes outside the device's magnetic planes [mx0, mx1)
+    // (constant: only magnetic cells evolve); empty when it is all zero,
+    // the normal case -- saves 3 doubles/cell of host memory on large grids
     std::vector<double> hostM;
     // timing
     int timing = 0;
@@ -507,7 +516,7 @@ int upload_probes(mpb_handle* h) {
             d.off = (int64_t)(L[0] - g.mx0) * g.PP + f;
         } else {
             d.ptr0 = d.ptr1 = nullptr;
-            d.constant =
+            d.constant = h->hostM.empty() ? 0.0 :
                 h->hostM[(((size_t)(comp - 6) * ncl + (L[0] - h->clo)) * ny + L[1]) * nz + L[2]];
         }
         pd[(size_t)p] = d;
@@ -740,7 +749,7 @@ int mpb_create(const mpb_setup* su, mpb_handle** out) {
             }
     }
     chk(dev_alloc(h, &h->probes, (size_t)std::max(1, h->nprobes)));
-    h->hostM.assign((size_t)3 * (h->chi - h->clo) * ny * nz, 0.0);
+    h->hostM.clear();
     if (rc) { mpb_destroy(h); return rc; }
     bool zero_id = true;
     for (int q = 0; q < 128; ++q) zero_id = zero_id && su->nccl_id[q] == 0;
@@ -804,7 +813,23 @@ int mpb_load_state(mpb_handle* h, const double* const fields[6], const double* m
         }
     const int ny = g.n[1], nz = g.n[2];
     const int ncl = h->chi - h->clo;
-    memcpy(h->hostM.data(), m, h->hostM.size() * sizeof(double));
+    {
+        const size_t plane = (size_t)ny * nz, total = (size_t)3 * ncl * plane;
+        bool zero = true;
+        for (int c = 0; c < 3 && zero; ++c)
+            for (int i = h->clo; i < h->chi && zero; ++i) {
+                if (h->mplanes && i >= g.mx0 && i < g.mx1) continue;   // on the device
+                const double* q = m + ((size_t)c * ncl + (i - h->clo)) * plane;
+                for (size_t e = 0; e < plane; ++e)
+                    if (dbits_host(q[e]) != 0) { zero = false; break; }
+            }
+        if (zero) {
+            h->hostM.clear();
+            h->hostM.shrink_to_fit();
+        } else {
+            h->hostM.assign(m, m + total);
+        }
+    }
     if (h->mplanes) {
         std::vector<double> pk((size_t)(h->mplanes * g.PP), 0.0);
         for (int c = 0; c < 3; ++c) {
@@ -840,7 +865,10 @@ int mpb_save_state(mpb_handle* h, double* const fields[6], double* m) {
     }
     const int ny = g.n[1], nz = g.n[2];
     const int ncl = h->chi - h->clo;
-    memcpy(m, h->hostM.data(), h->hostM.size() * sizeof(double));
+    if (h->hostM.empty())
+        memset(m, 0, sizeof(double) * (size_t)3 * ncl * ny * nz);
+    else
+        memcpy(m, h->hostM.data(), h->hostM.size() * sizeof(double));
     if (h->mplanes) {
         std::vector<double> pk((size_t)(h->mplanes * g.PP));
         for (int c = 0; c < 3; ++c) {

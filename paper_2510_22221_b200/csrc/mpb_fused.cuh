@@ -46,10 +46,38 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
     if (Fz == 1) sc.fz_magic = 0;   // j = f for Fz == 1 handled below
     // entries per CTA per plane: 2 per thread unless the plane is small
     fs->V = g.FyFz >= 8 * kSweepThreads * sms ? 4 : (g.FyFz >= 2 * kSweepThreads * 64 ? 2 : 1);
+    // mid-size 3D planes (C2, C3: ~17K entries) also take the two-CTA 256-thread
+    // form: measured +12-17% over one 512-thread CTA per SM
+    if (fs->V == 1 && g.act[0] && g.act[1] && g.act[2] && g.FyFz >= 2 * 256 * 16) fs->V = 2;
+    if (const char* e = getenv("MPB_SWEEP_V")) {
+        const int v = atoi(e);
+        if (v == 1 || v == 2 || v == 4) fs->V = v;
+    }
+    // staging ring bytes for a tile of T entries: 3 slots of E (T + both halo
+    // rows), H^n (T + low halo) and material ids
+    auto ring_bytes = [&](int T) {
+        const int ecap = (T + sc.hl + sc.eh + 4 + 1) & ~1;
+        const int hcap = (T + sc.hl + 4 + 1) & ~1;
+        const int icap = T + sc.hl + 48;
+        return (size_t)kSlots * (((3 * ecap + 3 * hcap) * 8 + icap + 127) / 128 * 128);
+    };
     // large 3D planes: 256-thread CTAs, two per SM (each one's barrier waits
-    // overlap the other's work); MPB_SWEEP_NT=512 selects one 512-thread CTA
+    // overlap the other's work) when two rings fit in the SM's shared memory
+    // (z-rows up to ~140 entries); longer rows take one 512-thread CTA per SM
+    // with a 1024-entry tile (C5: 2049x257 planes).  MPB_SWEEP_NT=512 forces
+    // the latter.
     fs->NT = kSweepThreads;
-    if (fs->V == 2 && g.act[0] && g.act[1] && g.act[2]) fs->NT = 256;
+    if (fs->V == 2 && g.act[0] && g.act[1] && g.act[2]) {
+        int smem_sm = 0, reserved = 0;
+        CU(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor,
+                                  h->device));
+        CU(cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock,
+                                  h->device));
+        cudaFuncAttributes fa{};
+        CU(cudaFuncGetAttributes(&fa, k_sweep<2, true, 256>));
+        const size_t per_cta = ring_bytes(2 * 256) + fa.sharedSizeBytes + (size_t)reserved;
+        if (2 * per_cta <= (size_t)smem_sm) fs->NT = 256;
+    }
     if (const char* e = getenv("MPB_SWEEP_NT"))
         if (atoi(e) == 512) fs->NT = kSweepThreads;
     sc.T = fs->V * fs->NT;
@@ -68,19 +96,21 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
     sc.hcap = (sc.T + sc.hl + 4 + 1) & ~1;
     sc.icap = sc.T + sc.hl + 48;
     sc.stage_bytes = ((3 * sc.ecap + 3 * sc.hcap) * 8 + sc.icap + 127) / 128 * 128;
-    sc.ring_offset = ((g.max_iters + 2) * 8 + 127) / 128 * 128;
-    fs->smem = (size_t)sc.ring_offset + (size_t)kSlots * sc.stage_bytes;
+    sc.ring_offset = 0;
+    fs->smem = (size_t)kSlots * sc.stage_bytes;
 
     const size_t static_smem = 8 * 1024;
     if (fs->smem + static_smem > (size_t)smem_optin)
         return fail_msg(MPB_EINVAL, "fused sweep staging (%zu B) exceeds shared memory",
                         fs->smem);
-    // x-chunks: ~8 waves of one CTA per SM, chunks of >= 24 planes
+    // x-chunks: ~32 (16) waves of two (one) CTAs per SM, chunks of >= 8 planes
     const int Fx = g.c1 - g.c0;                      // owned planes of this rank
     int waves = fs->NT == 256 ? 32 : 16;
     if (const char* e = getenv("MPB_SWEEP_WAVES")) waves = std::max(1, atoi(e));
     const int want = std::max(1, (waves * sms + sc.tiles - 1) / sc.tiles);
-    const int maxch = std::max(1, Fx / 24);
+    int minch = 8;   // >= 8 planes per chunk (pipeline fill is 3 planes)
+    if (const char* e = getenv("MPB_SWEEP_MINCHUNK")) minch = std::max(2, atoi(e));
+    const int maxch = std::max(1, Fx / minch);
     sc.nchunks = std::max(1, std::min(want, maxch));
     sc.chunk = (Fx + sc.nchunks - 1) / sc.nchunks;
     sc.nchunks = (Fx + sc.chunk - 1) / sc.chunk;

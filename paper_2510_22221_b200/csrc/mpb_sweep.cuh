@@ -82,7 +82,7 @@ struct SweepCfg {
     int icap;           // bytes of ids per slot
     uint32_t fz_magic;  // j = umulhi(f, magic) for f < FyFz
     int stage_bytes;    // bytes per ring slot
-    int ring_offset;    // bytes of dynamic smem before the ring (LLG history)
+    int ring_offset;    // bytes of dynamic smem before the ring (0)
     int nmat;           // entries of the material table
     int fastdiv;        // spacings within [2^-40, 2^10]: range-guarded divisions
     double rd[3];       // recip_of(d[a]) evaluated on the device at setup

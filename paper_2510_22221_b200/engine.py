@@ -56,8 +56,25 @@ def _codes(arr: np.ndarray, limit: int = 64):
     return codes.reshape(arr.shape), values, firsts
 
 
+def magnetic_count(materials) -> int:
+    if getattr(materials, "lazy", False):
+        return materials.magnetic_count()
+    return int(np.count_nonzero(np.asarray(materials.Ms) > 0.0))
+
+
 def material_table(materials, dt: float, spacings):
     """Per-cell uint8 ids and the coefficient table for ``materials``."""
+    if getattr(materials, "lazy", False):
+        # painted map: ids straight from the boxes, one row per distinct cell
+        ids, cells = materials.painted()
+        if len(cells) > N.MAX_MATERIALS:
+            raise ValueError(f"{len(cells)} distinct materials; the device table "
+                             f"holds at most {N.MAX_MATERIALS}")
+        col = lambda name: np.array([getattr(c, name) for c in cells], dtype=float)  # noqa: E731
+        hb = np.array([c.Hbias for c in cells], dtype=float).T
+        return ids, _table(col("sigma"), col("eps_r"), col("Ms"), col("alpha"),
+                           col("gamma_e"), [hb[c] for c in range(3)],
+                           col("Ms") > 0.0, dt, spacings)
     mag = np.asarray(materials.Ms) > 0.0
     fields = [np.asarray(materials.sigma), np.asarray(materials.eps_r)]
     mfields = [np.asarray(materials.Ms), np.asarray(materials.alpha),
@@ -90,6 +107,12 @@ def material_table(materials, dt: float, spacings):
     Ms, alpha, gamma = pick(mfields[0]), pick(mfields[1]), pick(mfields[2])
     hb = [pick(materials.Hbias[c]) for c in range(3)]
     ismag = pick(mag)
+    return ids, _table(sigma, eps_r, Ms, alpha, gamma, hb, ismag, dt, spacings)
+
+
+def _table(sigma, eps_r, Ms, alpha, gamma, hb, ismag, dt, spacings):
+    """Coefficient rows from per-material parameter vectors."""
+    nmat = len(sigma)
     # --- coefficients, reference expressions verbatim in meaning/order ---
     eps = CONSTANTS.eps0 * eps_r
     ca = 1.0 / (sigma / 2.0 + eps / dt)
@@ -111,7 +134,7 @@ def material_table(materials, dt: float, spacings):
             m.hbias[c] = hb[c][q]
         m.magnetic = int(bool(ismag[q]))
         m.eps = eps[q]
-    return ids, table
+    return table
 
 
 class DeviceRun:
@@ -165,7 +188,7 @@ class DeviceRun:
         su.graph_steps = graph_steps
         if slab is None:
             su.nranks, su.rank, su.x_lo, su.x_hi = 1, 0, 0, grid.nx
-            su.any_magnetic = int(np.count_nonzero(np.asarray(materials.Ms) > 0) > 0)
+            su.any_magnetic = int(magnetic_count(materials) > 0)
         else:
             su.nranks, su.rank = slab.nranks, slab.rank
             su.x_lo, su.x_hi = slab.x_lo, slab.x_hi
@@ -174,7 +197,7 @@ class DeviceRun:
         h = C.c_void_p()
         N.check(self.lib.mpb_create(C.byref(su), C.byref(h)))
         self.h = h
-        self.n_magnetic = int(np.count_nonzero(np.asarray(materials.Ms) > 0))
+        self.n_magnetic = magnetic_count(materials)
 
     # -- state ---------------------------------------------------------------
     def load_state(self, fields: dict, M: np.ndarray) -> None:

@@ -98,6 +98,8 @@ class FieldLattice:
 def initial_magnetization(materials: MaterialMap) -> np.ndarray:
     """M = Ms * unit(Hbias) in magnetic cells, +x where the bias is zero,
     0 elsewhere (grid.py:140-156); computed on the host once per run."""
+    if getattr(materials, "lazy", False):
+        return _initial_magnetization_painted(materials)
     M = np.zeros((3,) + tuple(materials.shape))
     mag = materials.magnetic_mask
     if mag.any():
@@ -108,6 +110,29 @@ def initial_magnetization(materials: MaterialMap) -> np.ndarray:
         unit[:, has] = hb[:, has] / norm[has]
         unit[0, ~has] = 1.0
         M[:, mag] = materials.Ms[mag] * unit
+    return M
+
+
+def _initial_magnetization_painted(materials) -> np.ndarray:
+    """initial_magnetization of a lazy map: the same per-cell expressions
+    evaluated once per distinct cell, then scattered by material id."""
+    ids, cells = materials.painted()
+    nc = len(cells)
+    hb = np.array([c.Hbias for c in cells], dtype=float).T.reshape(3, nc)
+    Ms = np.array([c.Ms for c in cells], dtype=float)
+    mag = Ms > 0.0
+    vec = np.zeros((3, nc))
+    if mag.any():
+        h = hb[:, mag]
+        norm = np.sqrt((h * h).sum(axis=0))
+        unit = np.zeros_like(h)
+        has = norm > 0
+        unit[:, has] = h[:, has] / norm[has]
+        unit[0, ~has] = 1.0
+        vec[:, mag] = Ms[mag] * unit
+    M = np.empty((3,) + tuple(materials.shape))
+    for c in range(3):
+        np.take(vec[c], ids, out=M[c])
     return M
 
 

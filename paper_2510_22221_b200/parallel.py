@@ -113,12 +113,21 @@ def nccl_unique_id(dist) -> bytes:
 class _MaterialSlab:
     """Cell-plane slice of a MaterialMap (what DeviceRun needs)."""
 
+    def __new__(cls, materials, slab: Slab):
+        if getattr(materials, "lazy", False):      # painted map: slice the boxes
+            return materials.region(*slab.cell_range)
+        return super().__new__(cls)
+
     def __init__(self, materials, slab: Slab):
         c0, c1 = slab.cell_range
         for name in ("sigma", "eps_r", "Ms", "alpha", "gamma_e"):
             setattr(self, name, np.asarray(getattr(materials, name))[c0:c1])
         self.Hbias = np.asarray(materials.Hbias)[:, c0:c1]
         self.shape = self.Ms.shape
+
+    @property
+    def magnetic_mask(self):
+        return self.Ms > 0.0
 
 
 def slab_device_runs(config, materials, keys, slabs, device=0, **kw):

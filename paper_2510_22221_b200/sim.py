@@ -80,6 +80,10 @@ class RunResult:
 
 def _materials_with_bias(materials, bias: float, direction) -> MaterialMap:
     """Copy with the magnetic cells' bias replaced (sim.py:82-97)."""
+    if getattr(materials, "lazy", False):
+        unit = np.asarray(direction, float)
+        unit = unit / np.linalg.norm(unit)
+        return materials.with_magnetic_bias([bias * unit[c] for c in range(3)])
     out = MaterialMap(materials.shape)
     for name in ("sigma", "eps_r", "Ms", "alpha", "gamma_e", "Hbias"):
         setattr(out, name, np.array(getattr(materials, name), copy=True))
