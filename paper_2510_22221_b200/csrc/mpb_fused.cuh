@@ -44,15 +44,6 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
                         g.FyFz);
     sc.fz_magic = (uint32_t)(((1ull << 32) + Fz - 1) / Fz);
     if (Fz == 1) sc.fz_magic = 0;   // j = f for Fz == 1 handled below
-    // entries per CTA per plane: 2 per thread unless the plane is small
-    fs->V = g.FyFz >= 8 * kSweepThreads * sms ? 4 : (g.FyFz >= 2 * kSweepThreads * 64 ? 2 : 1);
-    // mid-size 3D planes (C2, C3: ~17K entries) also take the two-CTA 256-thread
-    // form: measured +12-17% over one 512-thread CTA per SM
-    if (fs->V == 1 && g.act[0] && g.act[1] && g.act[2] && g.FyFz >= 2 * 256 * 16) fs->V = 2;
-    if (const char* e = getenv("MPB_SWEEP_V")) {
-        const int v = atoi(e);
-        if (v == 1 || v == 2 || v == 4) fs->V = v;
-    }
     // staging ring bytes for a tile of T entries: 3 slots of E (T + both halo
     // rows), H^n (T + low halo) and material ids
     auto ring_bytes = [&](int T) {
@@ -61,22 +52,33 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
         const int icap = T + sc.hl + 48;
         return (size_t)kSlots * (((3 * ecap + 3 * hcap) * 8 + icap + 127) / 128 * 128);
     };
-    // large 3D planes: 256-thread CTAs, two per SM (each one's barrier waits
-    // overlap the other's work) when two rings fit in the SM's shared memory
-    // (z-rows up to ~140 entries); longer rows take one 512-thread CTA per SM
-    // with a 1024-entry tile (C5: 2049x257 planes).  MPB_SWEEP_NT=512 forces
-    // the latter.
-    fs->NT = kSweepThreads;
-    if (fs->V == 2 && g.act[0] && g.act[1] && g.act[2]) {
-        int smem_sm = 0, reserved = 0;
-        CU(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor,
-                                  h->device));
-        CU(cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock,
-                                  h->device));
-        cudaFuncAttributes fa{};
-        CU(cudaFuncGetAttributes(&fa, k_sweep<2, true, 256>));
-        const size_t per_cta = ring_bytes(2 * 256) + fa.sharedSizeBytes + (size_t)reserved;
-        if (2 * per_cta <= (size_t)smem_sm) fs->NT = 256;
+    // Tile form, first that fits (V entries per thread, NT threads per CTA):
+    //  * 3D planes of >= 8K entries: V=2, NT=256, two CTAs per SM (each one's
+    //    barrier waits overlap the other's work) when two rings fit in the
+    //    SM's shared memory -- z-rows up to ~140 entries (C2, C3, C4);
+    //  * large planes with longer rows: V=2, NT=512, one CTA per SM with a
+    //    1024-entry tile (C5: 2049x257 planes);
+    //  * otherwise (small / 1D / 2D planes): V=1, NT=512.
+    // MPB_SWEEP_V / MPB_SWEEP_NT=512 override (experiments and tests).
+    int smem_sm = 0, reserved = 0;
+    CU(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, h->device));
+    CU(cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, h->device));
+    cudaFuncAttributes fa{};
+    CU(cudaFuncGetAttributes(&fa, k_sweep<2, true, 256>));
+    const size_t fixed = fa.sharedSizeBytes + (size_t)reserved;
+    const bool f3 = g.act[0] && g.act[1] && g.act[2];
+    if (f3 && g.FyFz >= 2 * 256 * 16 && 2 * (ring_bytes(512) + fixed) <= (size_t)smem_sm) {
+        fs->V = 2; fs->NT = 256;
+    } else if (g.FyFz >= 2 * kSweepThreads * 64 &&
+               ring_bytes(1024) + fixed <= (size_t)smem_optin) {
+        fs->V = 2; fs->NT = kSweepThreads;
+    } else {
+        fs->V = 1; fs->NT = kSweepThreads;
+    }
+    if (const char* e = getenv("MPB_SWEEP_V")) {
+        const int v = atoi(e);
+        if (v == 1 || v == 2 || v == 4) fs->V = v;
+        if (fs->V != 2) fs->NT = kSweepThreads;
     }
     if (const char* e = getenv("MPB_SWEEP_NT"))
         if (atoi(e) == 512) fs->NT = kSweepThreads;

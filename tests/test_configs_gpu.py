@@ -52,8 +52,10 @@ def mid_run_state(cfg, seed):
     return fields
 
 
-@pytest.mark.parametrize("name,steps", [("c2", 6), ("c3", 4)])
-def test_config_geometry_matches_oracle(name, steps):
+_ORACLE = {}
+
+
+def _case(name, steps):
     cfg = load_config(ROOT / "configs" / f"{name}.cfg")
     start = 200
     dt = orc.cfl_dt((cfg.grid.nx, cfg.grid.ny, cfg.grid.nz),
@@ -64,7 +66,14 @@ def test_config_geometry_matches_oracle(name, steps):
     snap = {"fields": mid_run_state(cfg, 7), "step": start,
             "probes": {k: np.zeros(start) for k in keys},
             "iterations": np.ones(start, dtype=int) if any_mag else np.zeros(0, dtype=int)}
-    ref = orc.run(cfg, resume={**snap, "fields": {k: v.copy() for k, v in snap["fields"].items()}})
+    if (name, steps) not in _ORACLE:
+        _ORACLE[(name, steps)] = orc.run(
+            cfg, resume={**snap, "fields": {k: v.copy() for k, v in snap["fields"].items()}})
+    return cfg, snap, _ORACLE[(name, steps)], any_mag, start
+
+
+def _check(name, steps):
+    cfg, snap, ref, any_mag, start = _case(name, steps)
     res = sim.run(cfg, resume=snap)
     assert res.steps == ref["steps"] == start + steps
     for k, v in ref["fields"].items():
@@ -75,3 +84,21 @@ def test_config_geometry_matches_oracle(name, steps):
         assert int(np.max(ref["iterations"][start:])) >= 2   # non-trivial fixed point
     for key, v in ref["probes"].items():
         assert np.array_equal(res.probes[key].samples, v), key
+
+
+@pytest.mark.parametrize("name,steps", [("c2", 6), ("c3", 4)])
+def test_config_geometry_matches_oracle(name, steps):
+    _check(name, steps)
+
+
+# every sweep instantiation (entries per thread V x CTA size NT) and odd tile
+# sizes must give the same bits: the tile shape is chosen per grid at setup
+@pytest.mark.parametrize("env", [
+    {"MPB_SWEEP_NT": "512"},                       # V=2, one 512-thread CTA per SM (C5 form)
+    {"MPB_SWEEP_V": "1"},                          # one entry per thread
+    {"MPB_SWEEP_T": "333", "MPB_SWEEP_MINCHUNK": "3"},   # ragged tiles and chunks
+])
+def test_sweep_tile_forms_match_oracle(env, monkeypatch):
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    _check("c2", 6)
