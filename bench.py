@@ -40,6 +40,13 @@ sys.path.insert(0, str(ROOT))
 
 CONFIGS = {"c1": "configs/c1.cfg", "c2": "configs/c2.cfg", "c3": "configs/c3.cfg",
            "c4": "configs/c4.cfg", "c5": "configs/c5.cfg"}
+DESCRIPTIONS = {
+    "c1": "vacuum PEC cavity + YIG block, 1000 Oe bias",
+    "c2": "CPW resonator on Si + YIG film, all-MUR1",
+    "c3": "standalone YIG film on Si, all-MUR1",
+    "c4": "CPW line on Si + YIG film, all-MUR1",
+    "c5": "CPW line on Si + YIG film, all-MUR1",
+}
 FALLBACK_HBM = 6650.0
 METRIC = "coupled Maxwell-LLG Gcell-updates/s"
 
@@ -442,7 +449,7 @@ def main() -> None:
         "config": {"workload": f"{args.config.upper()} {'x'.join(map(str, cfg.grid.cell_shape))} "
                                + ("cells per GPU" if args.scaling == "weak" else
                                   f"cells split over {world} GPU(s)")
-                               + ", CPW + YIG film, all-MUR1, fp64",
+                               + f", {DESCRIPTIONS[args.config]}, fp64",
                    "config_file": CONFIGS[args.config], "cells_per_gpu": rank_cells,
                    "cells_total": total_cells,
                    "magnetic_fraction": f_mag,
