@@ -74,3 +74,17 @@ def test_lazy_region_and_bias_override():
     bl = _materials_with_bias(lazy.materials, 2.5e4, (0.0, 1.0, 1.0))
     assert bl.lazy
     assert same(initial_magnetization(bd), initial_magnetization(bl))
+
+
+@pytest.mark.parametrize("c0,c1", [(0, 65), (63, 130), (127, 257), (1, 2), (200, 600)])
+def test_tiled_region_is_periodic_slice(c0, c1):
+    """Weak-scaling slabs (bench.py): the config repeated along x."""
+    dense = load_config(ROOT / "configs" / "c2.cfg")
+    lazy = load_config(ROOT / "configs" / "c2.cfg", lazy=True)
+    nx = dense.grid.nx
+    period = np.arange(c0, c1) % nx
+    t = lazy.materials.tiled_region(c0, c1)
+    assert t.shape == (c1 - c0,) + dense.materials.shape[1:]
+    for f in ("sigma", "eps_r", "Ms", "alpha", "gamma_e"):
+        assert same(np.asarray(getattr(t, f)), np.asarray(getattr(dense.materials, f))[period]), f
+    assert same(np.asarray(t.Hbias), np.asarray(dense.materials.Hbias)[:, period])
