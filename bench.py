@@ -458,7 +458,7 @@ def main() -> None:
                    "kernel_variant": args.variant,
                    "initial_state": args.init},
         "e2e": {"value": e2e, "unit": "Gcell-updates/s",
-                "h2d_bytes_per_step": 8, "d2h_bytes_per_step": 8 * len(keys) + 4,
+                "h2d_bytes_per_step": 8, "d2h_bytes_per_step": 8 * len(dev.probes) + 4,
                 "api": "mpb_run (host source values in, host probes + r* out)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak if achieved else None,
