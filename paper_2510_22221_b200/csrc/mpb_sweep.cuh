@@ -224,7 +224,7 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
     auto sI = [&](int s) {
         return ring + (size_t)s * sc.stage_bytes + (3 * sc.ecap + 3 * sc.hcap) * 8;
     };
-    auto issue = [&](int p) {   // thread 0 only
+    auto issue = [&](int p) {   // issuing thread only
         const int s = slot(p);
         const bool full = p < i1;
         const uint32_t bytes = 3 * ebytes + (full ? 3 * hbytes + ibytes : 0u);
@@ -237,7 +237,11 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
             tma_load_1d(sI(s), gids + base + ia0, ibytes, &bars[s]);
         }
     };
-    if (tid == 0)
+    // the refills are issued by lane 0 of the LAST warp: the strided H loop
+    // gives low thread ids the extra (halo) entries, so the last warp has
+    // slack to absorb the issue time before the plane barrier
+    constexpr int kIssuer = NT - 32;
+    if (tid == kIssuer)
         for (int p = pstart; p <= plast && p < pstart + kSlots; ++p) issue(p);
 
     // reciprocals of the spacings: recip_of() evaluated once at setup on the
@@ -290,7 +294,7 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
         // H^{n+1}(p) complete everywhere, and every thread is past E(p-1) and
         // H(p), the last readers of plane p-1's slot: refill it with p+2
         __syncthreads();
-        if (tid == 0 && p > pstart && p + 2 <= plast) {
+        if (tid == kIssuer && p > pstart && p + 2 <= plast) {
             fence_proxy_async();
             issue(p + 2);
         }
