@@ -140,8 +140,9 @@ MPB_API void mpb_destroy(mpb_handle* h);
 
 /* Upload / download the full state in reference layout
  * (FieldLattice.load_state / state_arrays, grid.py:125-137).
- * fields[0..5] = Ex Ey Ez Hx Hy Hz, each prod(field_shape) doubles;
- * m = 3*nx*ny*nz doubles. */
+ * fields[0..5] = Ex Ey Ez Hx Hy Hz, each prod(field_shape) doubles
+ * (mpb_load_state: a NULL entry loads that component as all zeros, the
+ * reference's fresh-run state, without a host array); m = 3*nx*ny*nz doubles. */
 MPB_API int mpb_load_state(mpb_handle* h, const double* const fields[6], const double* m);
 MPB_API int mpb_save_state(mpb_handle* h, double* const fields[6], double* m);
 

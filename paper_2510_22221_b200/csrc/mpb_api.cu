@@ -805,12 +805,19 @@ int mpb_load_state(mpb_handle* h, const double* const fields[6], const double* m
     CU(cudaStreamSynchronize(h->stream));
     const size_t row = (size_t)g.FyFz * sizeof(double);
     const int nplanes = h->hi - h->lo;
-    for (int p = 0; p < 2; ++p)
-        for (int c = 0; c < 6; ++c) {
-            double* dst = c < 3 ? h->E[p][c] : h->H[p][c - 3];
-            CU(cudaMemcpy2D(dst, g.PP * sizeof(double), fields[c], row, row, nplanes,
+    const size_t whole = (size_t)nplanes * g.PP * sizeof(double);
+    for (int c = 0; c < 6; ++c) {
+        double* d0 = c < 3 ? h->E[0][c] : h->H[0][c - 3];
+        double* d1 = c < 3 ? h->E[1][c] : h->H[1][c - 3];
+        if (fields[c]) {   // upload once, replicate into the second buffer set
+            CU(cudaMemcpy2D(d0, g.PP * sizeof(double), fields[c], row, row, nplanes,
                             cudaMemcpyHostToDevice));
+            CU(cudaMemcpy(d1, d0, whole, cudaMemcpyDeviceToDevice));
+        } else {           // NULL: the component starts at zero
+            CU(cudaMemset(d0, 0, whole));
+            CU(cudaMemset(d1, 0, whole));
         }
+    }
     const int ny = g.n[1], nz = g.n[2];
     const int ncl = h->chi - h->clo;
     {

@@ -186,9 +186,10 @@ class DeviceRun:
         su.device = device
         su.kernel_variant = kernel_variant
         su.graph_steps = graph_steps
+        n_magnetic = magnetic_count(materials)
         if slab is None:
             su.nranks, su.rank, su.x_lo, su.x_hi = 1, 0, 0, grid.nx
-            su.any_magnetic = int(magnetic_count(materials) > 0)
+            su.any_magnetic = int(n_magnetic > 0)
         else:
             su.nranks, su.rank = slab.nranks, slab.rank
             su.x_lo, su.x_hi = slab.x_lo, slab.x_hi
@@ -197,19 +198,24 @@ class DeviceRun:
         h = C.c_void_p()
         N.check(self.lib.mpb_create(C.byref(su), C.byref(h)))
         self.h = h
-        self.n_magnetic = magnetic_count(materials)
+        self.n_magnetic = n_magnetic
 
     # -- state ---------------------------------------------------------------
-    def load_state(self, fields: dict, M: np.ndarray) -> None:
-        arrs = [np.ascontiguousarray(fields[n], dtype=np.float64) for n in E_H_NAMES]
-        for a in arrs:
-            if a.shape != self.fs:
-                raise ValueError("snapshot shape mismatch")
+    def load_state(self, fields: dict | None, M: np.ndarray) -> None:
+        """``fields`` None: E and H start at zero (no host arrays)."""
+        if fields is None:
+            arrs = [None] * 6
+        else:
+            arrs = [np.ascontiguousarray(fields[n], dtype=np.float64) for n in E_H_NAMES]
+            for a in arrs:
+                if a.shape != self.fs:
+                    raise ValueError("snapshot shape mismatch")
         m = np.ascontiguousarray(M, dtype=np.float64)
         if m.shape != (3,) + tuple(self.n):
             raise ValueError("snapshot shape mismatch for M")
         ptrs = (C.POINTER(C.c_double) * 6)(
-            *[a.ctypes.data_as(C.POINTER(C.c_double)) for a in arrs])
+            *[a.ctypes.data_as(C.POINTER(C.c_double)) if a is not None else None
+              for a in arrs])
         N.check(self.lib.mpb_load_state(self.h, ptrs,
                                         m.ctypes.data_as(C.POINTER(C.c_double))))
 

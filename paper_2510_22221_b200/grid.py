@@ -67,6 +67,23 @@ class FieldLattice:
             setattr(self, name, np.zeros(spec.field_shape))
         self.M = np.zeros((3,) + spec.cell_shape)
 
+    @classmethod
+    def adopt(cls, spec: GridSpec, materials, state: dict) -> "FieldLattice":
+        """Lattice that takes ownership of freshly downloaded state arrays
+        (no copy; same checks as load_state)."""
+        lat = cls.__new__(cls)
+        lat.spec = spec
+        lat.materials = materials
+        for name in E_NAMES + H_NAMES:
+            a = state[name]
+            if a.shape != spec.field_shape or a.dtype != np.float64:
+                raise ValueError(f"snapshot shape mismatch for {name}")
+            setattr(lat, name, a)
+        if state["M"].shape != (3,) + spec.cell_shape:
+            raise ValueError("snapshot shape mismatch for M")
+        lat.M = state["M"]
+        return lat
+
     def field(self, name: str) -> np.ndarray:
         if name in E_NAMES or name in H_NAMES:
             return getattr(self, name)
@@ -118,6 +135,9 @@ def _initial_magnetization_painted(materials) -> np.ndarray:
     evaluated once per distinct cell, then scattered by material id."""
     ids, cells = materials.painted()
     nc = len(cells)
+    M = np.zeros((3,) + tuple(materials.shape))
+    if not any(c.Ms > 0.0 for c in cells):
+        return M
     hb = np.array([c.Hbias for c in cells], dtype=float).T.reshape(3, nc)
     Ms = np.array([c.Ms for c in cells], dtype=float)
     mag = Ms > 0.0
@@ -130,9 +150,11 @@ def _initial_magnetization_painted(materials) -> np.ndarray:
         unit[:, has] = h[:, has] / norm[has]
         unit[0, ~has] = 1.0
         vec[:, mag] = Ms[mag] * unit
-    M = np.empty((3,) + tuple(materials.shape))
+    # scatter into the magnetic cells only (a few % of the grid)
+    where = np.flatnonzero(mag[ids])
+    q = ids.reshape(-1)[where]
     for c in range(3):
-        np.take(vec[c], ids, out=M[c])
+        M[c].reshape(-1)[where] = vec[c][q]
     return M
 
 

@@ -170,9 +170,7 @@ def run(config: SimConfig, bias: float | None = None, resume: dict | None = None
             st = resume["fields"]
             dev.load_state({n: st[n] for n in _FIELD_NAMES}, st["M"])
         else:
-            zeros = np.zeros(config.grid.field_shape)
-            dev.load_state({n: zeros for n in _FIELD_NAMES},
-                           initial_magnetization(materials))
+            dev.load_state(None, initial_magnetization(materials))   # E = H = 0
         count = max(0, n_steps - start)
         vals = source_values(config.source, dt, start, n_steps)
         probe_rows, iters, fail = dev.run(start, vals)
@@ -189,8 +187,7 @@ def run(config: SimConfig, bias: float | None = None, resume: dict | None = None
         state = dev.save_state()
     finally:
         dev.close()
-    lat = FieldLattice(config.grid, materials)
-    lat.load_state(state)
+    lat = FieldLattice.adopt(config.grid, materials, state)
     b = 0.0 if bias is None else bias
     probes = {}
     for p, key in enumerate(keys):
@@ -259,6 +256,19 @@ def _sweep_one(args):
     return spec.freqs, spec.mags
 
 
+def _sweep_device(args):
+    """All biases assigned to one GPU, ``streams`` of them at a time: each run
+    owns a handle with its own CUDA stream, driven from its own host thread
+    (the C ABI releases the GIL), so small grids that cannot fill a B200 on
+    their own share it."""
+    jobs, streams = args
+    if streams <= 1 or len(jobs) <= 1:
+        return [_sweep_one(j) for j in jobs]
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=streams) as ex:
+        return list(ex.map(_sweep_one, jobs))
+
+
 def _gpu_count() -> int:
     try:
         import torch
@@ -270,21 +280,30 @@ def _gpu_count() -> int:
 def sweep(config: SimConfig, biases=None, parallel: int = 1) -> SpectrumMap:
     """Hann-window FFT magnitude of the spectrum probe for every bias.
 
-    ``parallel > 1`` runs up to ``parallel`` biases at once, one process per
-    GPU (spawned, never forked after CUDA init).  Rows are assembled in bias
-    order, so serial and parallel sweeps are identical (reference
-    sim.py:243-260).
+    ``parallel > 1`` runs up to ``parallel`` biases at once: spread over the
+    GPUs (one spawned process per GPU, never forked after CUDA init) and, when
+    ``parallel`` exceeds the GPU count, several concurrent runs per GPU on
+    separate streams.  Every run is independent and deterministic, and rows
+    are assembled in bias order, so serial and parallel sweeps are identical
+    (reference sim.py:243-260).
     """
     biases = np.asarray(config.bias_sweep if biases is None else biases, float)
     if biases.size == 0:
         raise ValueError("bias sweep must be non-empty")
     ngpu = max(1, _gpu_count())
-    workers = max(1, min(parallel, ngpu, biases.size))
-    jobs = [(config, float(b), i % workers) for i, b in enumerate(biases)]
-    if workers > 1:
+    parallel = max(1, min(int(parallel), biases.size))
+    gpus = min(parallel, ngpu)
+    streams = -(-parallel // gpus)                       # concurrent runs per GPU
+    per_gpu = [[] for _ in range(gpus)]
+    order = []
+    for i, b in enumerate(biases):
+        per_gpu[i % gpus].append((config, float(b), i % gpus))
+        order.append((i % gpus, len(per_gpu[i % gpus]) - 1))
+    if gpus > 1:
         import multiprocessing as mp
-        with mp.get_context("spawn").Pool(workers) as pool:
-            rows = pool.map(_sweep_one, jobs)
+        with mp.get_context("spawn").Pool(gpus) as pool:
+            done = pool.map(_sweep_device, [(jobs, streams) for jobs in per_gpu])
     else:
-        rows = [_sweep_one(j) for j in jobs]
+        done = [_sweep_device((per_gpu[0], streams))]
+    rows = [done[g][q] for g, q in order]
     return SpectrumMap(biases=biases, freqs=rows[0][0], mags=np.stack([r[1] for r in rows]))

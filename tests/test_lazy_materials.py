@@ -37,7 +37,7 @@ def same(a, b):
 
 @pytest.mark.parametrize("name", ["c1", "c2", "c3"])
 def test_lazy_map_matches_dense(name):
-    dense = load_config(ROOT / "configs" / f"{name}.cfg")
+    dense = load_config(ROOT / "configs" / f"{name}.cfg", lazy=False)
     lazy = load_config(ROOT / "configs" / f"{name}.cfg", lazy=True)
     assert lazy.materials.lazy and not lazy.materials.dense
     g = dense.grid
@@ -58,7 +58,7 @@ def test_lazy_map_matches_dense(name):
 
 
 def test_lazy_region_and_bias_override():
-    dense = load_config(ROOT / "configs" / "c3.cfg")
+    dense = load_config(ROOT / "configs" / "c3.cfg", lazy=False)
     lazy = load_config(ROOT / "configs" / "c3.cfg", lazy=True)
     g = dense.grid
     sp = (g.dx, g.dy, g.dz)
@@ -79,7 +79,7 @@ def test_lazy_region_and_bias_override():
 @pytest.mark.parametrize("c0,c1", [(0, 65), (63, 130), (127, 257), (1, 2), (200, 600)])
 def test_tiled_region_is_periodic_slice(c0, c1):
     """Weak-scaling slabs (bench.py): the config repeated along x."""
-    dense = load_config(ROOT / "configs" / "c2.cfg")
+    dense = load_config(ROOT / "configs" / "c2.cfg", lazy=False)
     lazy = load_config(ROOT / "configs" / "c2.cfg", lazy=True)
     nx = dense.grid.nx
     period = np.arange(c0, c1) % nx

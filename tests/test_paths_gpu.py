@@ -86,6 +86,10 @@ def test_sweep_matches_oracle_spectra(tmp_path):
         x = list(ref["probes"].values())[cfg.spectrum_probe]
         spec = fft_magnitude((x, ref["dt"]), window="hann")
         assert np.array_equal(row, spec.mags)
+    # several concurrent runs per GPU (separate streams, host threads):
+    # identical rows, in bias order
+    par = sim.sweep(cfg, parallel=3)
+    assert np.array_equal(par.mags, smap.mags) and np.array_equal(par.freqs, smap.freqs)
 
 
 @pytest.mark.parametrize("name", ["mixed3d", "allmur3d", "pec_block"])
