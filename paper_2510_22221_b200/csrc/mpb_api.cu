@@ -103,6 +103,12 @@ struct mpb_handle {
     int64_t stage_cap = 0;
     cudaStream_t stream = nullptr;
     cudaGraphExec_t graph[2] = {nullptr, nullptr};
+    // slab exchange overlapped with the next step's interior sweep: the
+    // exchange runs on comm_stream after ev_post, the edge chunks wait ev_exch
+    bool overlap = false;
+    bool exch_pending = false;
+    cudaStream_t comm_stream = nullptr;
+    cudaEvent_t ev_post = nullptr, ev_exch = nullptr;
     // host copy of M on the local cell planes (cells outside the device M
     // range never change)
     // M of the cell planes outside the device's magnetic planes [mx0, mx1)
@@ -123,7 +129,8 @@ namespace {
 // Fused single-sweep variant hooks (mpb_fused.cuh).
 int prepare_fused(mpb_handle* h, const Geom& g);
 void destroy_fused(mpb_handle* h);
-int launch_fused(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s);
+int launch_fused(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s, int part,
+                 int64_t& launches);
 int launch_deferred(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s);
 int launch_zfix(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s);
 int zfix_launches(mpb_handle* h);
@@ -212,22 +219,45 @@ int exchange(mpb_handle* h, int pb, cudaStream_t s) {
 
 // ---- step phases (shared by the NCCL path and the in-process group) ----
 
-int phase_sweep(mpb_handle* h, int pa, cudaStream_t s, int64_t& launches) {
+// part 0: whole sweep + LLG; 1: interior chunks only (overlaps the slab
+// exchange of the previous step); 2: edge chunks + LLG (after the exchange).
+int phase_sweep(mpb_handle* h, int pa, cudaStream_t s, int64_t& launches, int part = 0) {
     const Geom& g = h->g;
     const Bufs b = make_bufs(h, pa);
     const size_t hist_smem = (size_t)(g.max_iters + 2) * sizeof(unsigned long long);
     const dim3 plane_grid((g.FyFz + 255) / 256, g.c1 - g.c0);
     if (h->variant == 1) {
         k_hsweep<<<plane_grid, 256, hist_smem, s>>>(g, b, h->mats, ids_view(h), h->st);
-    } else {
-        int rc = launch_fused(h, g, b, s);
-        if (rc) return rc;
-        if (h->nmag > 0) {
-            if ((rc = launch_llg_local(h, g, b, s))) return rc;
-            ++launches;
-        }
+        ++launches;
+        return MPB_OK;
     }
-    ++launches;
+    int rc = launch_fused(h, g, b, s, part, launches);
+    if (rc) return rc;
+    if (part != 1 && h->nmag > 0) {
+        if ((rc = launch_llg_local(h, g, b, s))) return rc;
+        ++launches;
+    }
+    return MPB_OK;
+}
+
+// Sweep of a slab step: when the previous step's boundary exchange is still
+// in flight on the comm stream, the interior chunks run first and only the
+// edge chunks wait for it (exchange overlapped with the interior).
+int phase_sweep_overlapped(mpb_handle* const* hs, int n, int pa, cudaStream_t s,
+                           int64_t& launches) {
+    int rc;
+    mpb_handle* h0 = hs[0];
+    if (!h0->exch_pending) {
+        for (int r = 0; r < n; ++r)
+            if ((rc = phase_sweep(hs[r], pa, s, launches, 0))) return rc;
+        return MPB_OK;
+    }
+    for (int r = 0; r < n; ++r)
+        if ((rc = phase_sweep(hs[r], pa, s, launches, 1))) return rc;
+    CU(cudaStreamWaitEvent(s, h0->ev_exch, 0));
+    h0->exch_pending = false;
+    for (int r = 0; r < n; ++r)
+        if ((rc = phase_sweep(hs[r], pa, s, launches, 2))) return rc;
     return MPB_OK;
 }
 
@@ -316,7 +346,7 @@ int enqueue_step(mpb_handle* h, int pa, bool timed) {
         CU(cudaEventCreate(&e1));
         CU(cudaEventRecord(e0, s));
     }
-    if ((rc = phase_sweep(h, pa, s, launches))) return rc;
+    if ((rc = phase_sweep_overlapped(&h, 1, pa, s, launches))) return rc;
     if (timed) {
         CU(cudaEventRecord(e1, s));
         h->events.emplace_back(e0, e1);
@@ -351,7 +381,15 @@ int enqueue_step(mpb_handle* h, int pa, bool timed) {
         if ((rc = phase_post(h, pa, s, launches))) return rc;
     }
     if (h->nranks > 1) {
-        if ((rc = exchange(h, 1 - pa, s))) return rc;
+        if (h->overlap) {   // on the comm stream, overlapping the next interior sweep
+            CU(cudaEventRecord(h->ev_post, s));
+            CU(cudaStreamWaitEvent(h->comm_stream, h->ev_post, 0));
+            if ((rc = exchange(h, 1 - pa, h->comm_stream))) return rc;
+            CU(cudaEventRecord(h->ev_exch, h->comm_stream));
+            h->exch_pending = true;
+        } else if ((rc = exchange(h, 1 - pa, s))) {
+            return rc;
+        }
     }
     h->launches_last += launches;
     CU(cudaGetLastError());
@@ -391,8 +429,7 @@ int exchange_group(mpb_handle* const* hs, int n, int pb, cudaStream_t s) {
 int group_step(mpb_handle* const* hs, int n, int pa, cudaStream_t s) {
     int rc;
     int64_t launches = 0;
-    for (int r = 0; r < n; ++r)
-        if ((rc = phase_sweep(hs[r], pa, s, launches))) return rc;
+    if ((rc = phase_sweep_overlapped(hs, n, pa, s, launches))) return rc;
     if (hs[0]->any_magnetic) {
         StatePtrs sp{};
         sp.n = n;
@@ -406,8 +443,26 @@ int group_step(mpb_handle* const* hs, int n, int pa, cudaStream_t s) {
     }
     for (int r = 0; r < n; ++r)
         if ((rc = phase_post(hs[r], pa, s, launches))) return rc;
-    if ((rc = exchange_group(hs, n, 1 - pa, s))) return rc;
+    if (hs[0]->overlap) {   // device copies on the comm stream, like exchange()
+        mpb_handle* h0 = hs[0];
+        CU(cudaEventRecord(h0->ev_post, s));
+        CU(cudaStreamWaitEvent(h0->comm_stream, h0->ev_post, 0));
+        if ((rc = exchange_group(hs, n, 1 - pa, h0->comm_stream))) return rc;
+        CU(cudaEventRecord(h0->ev_exch, h0->comm_stream));
+        h0->exch_pending = true;
+    } else if ((rc = exchange_group(hs, n, 1 - pa, s))) {
+        return rc;
+    }
     CU(cudaGetLastError());
+    return MPB_OK;
+}
+
+// Make `s` wait for a boundary exchange still in flight (end of a run).
+int drain_exchange(mpb_handle* h, cudaStream_t s) {
+    if (h->exch_pending) {
+        CU(cudaStreamWaitEvent(s, h->ev_exch, 0));
+        h->exch_pending = false;
+    }
     return MPB_OK;
 }
 
@@ -459,7 +514,7 @@ int enqueue_steps(mpb_handle* h, int64_t nsteps) {
             ++s;
         }
     }
-    return MPB_OK;
+    return drain_exchange(h, h->stream);
 }
 
 int set_run_buffers(mpb_handle* h, int64_t n0, const double* src, double* probe,
@@ -594,6 +649,13 @@ int mpb_create(const mpb_setup* su, mpb_handle** out) {
     h->rank = nranks == 1 ? 0 : su->rank;
     CU(cudaSetDevice(h->device));
     CU(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    if (nranks > 1) {
+        CU(cudaStreamCreateWithFlags(&h->comm_stream, cudaStreamNonBlocking));
+        CU(cudaEventCreateWithFlags(&h->ev_post, cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&h->ev_exch, cudaEventDisableTiming));
+        const char* e = getenv("MPB_OVERLAP");
+        h->overlap = su->kernel_variant != 1 && !(e && atoi(e) == 0);
+    }
 
     Geom& g = h->g;
     int64_t F[3];
@@ -793,6 +855,9 @@ void mpb_destroy(mpb_handle* h) {
     cudaFree(h->d_iters);
     destroy_fused(h);
     if (h->comm) ncclCommDestroy(h->comm);
+    if (h->ev_post) cudaEventDestroy(h->ev_post);
+    if (h->ev_exch) cudaEventDestroy(h->ev_exch);
+    if (h->comm_stream) cudaStreamDestroy(h->comm_stream);
     if (h->stream) cudaStreamDestroy(h->stream);
     delete h;
 }
@@ -1056,6 +1121,7 @@ int mpb_group_run(mpb_handle* const* hs, int32_t n, int64_t n0, int64_t nsteps,
         rc = group_step(hs, n, hs[0]->parity, s);
         for (int r = 0; r < n; ++r) hs[r]->parity ^= 1;
     }
+    if (!rc) rc = drain_exchange(hs[0], s);
     if (!rc) {
         CU(cudaStreamSynchronize(s));
         for (int r = 0; r < n; ++r)

@@ -116,6 +116,8 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
     sc.nchunks = std::max(1, std::min(want, maxch));
     sc.chunk = (Fx + sc.nchunks - 1) / sc.nchunks;
     sc.nchunks = (Fx + sc.chunk - 1) / sc.chunk;
+    sc.ch_base = 0;
+    sc.ch_step = 1;
     fs->grid = sc.tiles * sc.nchunks;
     fs->F3 = g.act[0] && g.act[1] && g.act[2];
     int rc;
@@ -218,14 +220,29 @@ void destroy_fused(mpb_handle* h) {
     h->fused = nullptr;
 }
 
-int launch_fused(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s) {
+// part 0: every x-chunk; 1: the interior chunks (no ghost plane read or
+// written); 2: the first and last chunk (the only ones touching the ghost
+// planes a slab exchange fills).  Adds the launches made to `launches`.
+int launch_fused(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s, int part,
+                 int64_t& launches) {
     FusedState* fs = fused_of(h);
+    SweepCfg sc = fs->sc;
+    int grid = fs->grid;
+    if (part == 1) {
+        if (sc.nchunks <= 2) return MPB_OK;
+        sc.ch_base = 1;
+        grid = sc.tiles * (sc.nchunks - 2);
+    } else if (part == 2) {
+        sc.ch_step = std::max(1, sc.nchunks - 1);
+        grid = sc.tiles * std::min(2, sc.nchunks);
+    }
+    ++launches;
 #define MPB_LAUNCH(VV, FF)                                                              \
-    k_sweep<VV, FF><<<fs->grid, kSweepThreads, fs->smem, s>>>(g, b, h->mats, ids_view(h), \
-                                                              h->st, fs->sc)
+    k_sweep<VV, FF><<<grid, kSweepThreads, fs->smem, s>>>(g, b, h->mats, ids_view(h),     \
+                                                          h->st, sc)
     if (fs->NT == 256) {
-        k_sweep<2, true, 256><<<fs->grid, 256, fs->smem, s>>>(g, b, h->mats, ids_view(h), h->st,
-                                                             fs->sc);
+        k_sweep<2, true, 256><<<grid, 256, fs->smem, s>>>(g, b, h->mats, ids_view(h), h->st,
+                                                         sc);
     } else if (fs->F3) {
         if (fs->V == 4) MPB_LAUNCH(4, true);
         else if (fs->V == 2) MPB_LAUNCH(2, true);

@@ -83,6 +83,8 @@ struct SweepCfg {
     uint32_t fz_magic;  // j = umulhi(f, magic) for f < FyFz
     int stage_bytes;    // bytes per ring slot
     int ring_offset;    // bytes of dynamic smem before the ring (0)
+    int ch_base;        // chunk of blockIdx.x / tiles == 0 (launch subsets)
+    int ch_step;        // chunk stride between consecutive block rows
     int nmat;           // entries of the material table
     int fastdiv;        // spacings within [2^-40, 2^10]: range-guarded divisions
     double rd[3];       // recip_of(d[a]) evaluated on the device at setup
@@ -177,7 +179,7 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
     if (st->fail) return;
     const int tid = threadIdx.x;
     const int tile = blockIdx.x % sc.tiles;
-    const int chunk = blockIdx.x / sc.tiles;
+    const int chunk = sc.ch_base + (blockIdx.x / sc.tiles) * sc.ch_step;
     const int f0 = tile * sc.T;
     const int f1 = min(f0 + sc.T, g.FyFz);
     const int Fx = g.F[0];

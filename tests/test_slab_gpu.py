@@ -30,3 +30,16 @@ def test_slab_group_matches_reference_golden(name, nranks):
     assert np.array_equal(its, g["iterations"])
     for key, v in g["probes"].items():
         assert np.array_equal(probes[key], v), key
+
+
+# Short x-chunks (2 planes) give every slab >= 3 chunks, so the overlapped
+# path really splits each sweep into interior chunks (running while the
+# previous step's boundary copies are in flight on the comm stream) and edge
+# chunks (after them); MPB_OVERLAP=0 is the serialised order.
+@pytest.mark.parametrize("overlap", ["1", "0"])
+@pytest.mark.parametrize("name,nranks", [("mixed3d", 2), ("pec_block", 2), ("bias3d", 2),
+                                         ("allmur3d", 2)])
+def test_slab_overlapped_exchange_matches_golden(name, nranks, overlap, monkeypatch):
+    monkeypatch.setenv("MPB_SWEEP_MINCHUNK", "2")
+    monkeypatch.setenv("MPB_OVERLAP", overlap)
+    test_slab_group_matches_reference_golden(name, nranks)
