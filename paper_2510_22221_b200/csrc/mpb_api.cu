@@ -778,6 +778,14 @@ int mpb_create(const mpb_setup* su, mpb_handle** out) {
         const int need = (h->nmag + 255) / 256;
         h->fixup_blocks = std::max(1, std::min(need, per_sm * sms));
     }
+    {   // reciprocals of the spacings for the exact-division fast path
+        double* dr = nullptr;
+        CU(cudaMalloc(&dr, 3 * sizeof(double)));
+        k_recips<<<1, 1>>>(g.d[0], g.d[1], g.d[2], dr);
+        CU(cudaGetLastError());
+        CU(cudaMemcpy(g.rd, dr, 3 * sizeof(double), cudaMemcpyDeviceToHost));
+        cudaFree(dr);
+    }
     if (h->variant != 1) {
         rc = prepare_fused(h, g);
         if (rc) { mpb_destroy(h); return rc; }

@@ -131,12 +131,7 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
                         : (fs->V == 2 ? set_smem_attr<2, false>(fs->smem) : set_smem_attr<1, false>(fs->smem));
     if (rc) return rc;
     {   // reciprocals of the spacings, computed once on the device
-        double* dr = nullptr;
-        CU(cudaMalloc(&dr, 3 * sizeof(double)));
-        k_recips<<<1, 1>>>(g.d[0], g.d[1], g.d[2], dr);
-        CU(cudaGetLastError());
-        CU(cudaMemcpy(sc.rd, dr, 3 * sizeof(double), cudaMemcpyDeviceToHost));
-        cudaFree(dr);
+        for (int a = 0; a < 3; ++a) sc.rd[a] = g.rd[a];   // set in mpb_create
     }
     if (rc) return rc;
     // deferred E entries: {c, c+x, c+y, c+z} over magnetic cells

@@ -121,16 +121,16 @@ __device__ __forceinline__ E3 e_plain_at(const Geom& g, const Bufs& b,
                        g.faces[2] == MPB_FACE_PMC, g.faces[3] == MPB_FACE_PMC,
                        g.faces[4] == MPB_FACE_PMC, g.faces[5] == MPB_FACE_PMC};
     if (g.act[1]) {   // cHx += dHz/dy ; cHz -= dHx/dy
-        cx = cx + bwd_diff(H[2], o, sy, j, g.n[1], g.d[1], p[2], p[3]);
-        cz = cz - bwd_diff(H[0], o, sy, j, g.n[1], g.d[1], p[2], p[3]);
+        cx = cx + bwd_diff(H[2], o, sy, j, g.n[1], g.d[1], g.rd[1], p[2], p[3]);
+        cz = cz - bwd_diff(H[0], o, sy, j, g.n[1], g.d[1], g.rd[1], p[2], p[3]);
     }
     if (g.act[2]) {   // cHx -= dHy/dz ; cHy += dHx/dz
-        cx = cx - bwd_diff(H[1], o, 1, k, g.n[2], g.d[2], p[4], p[5]);
-        cy = cy + bwd_diff(H[0], o, 1, k, g.n[2], g.d[2], p[4], p[5]);
+        cx = cx - bwd_diff(H[1], o, 1, k, g.n[2], g.d[2], g.rd[2], p[4], p[5]);
+        cy = cy + bwd_diff(H[0], o, 1, k, g.n[2], g.d[2], g.rd[2], p[4], p[5]);
     }
     if (g.act[0]) {   // cHy -= dHz/dx ; cHz += dHy/dx
-        cy = cy - bwd_diff(H[2], o, sx, i, g.n[0], g.d[0], p[0], p[1]);
-        cz = cz + bwd_diff(H[1], o, sx, i, g.n[0], g.d[0], p[0], p[1]);
+        cy = cy - bwd_diff(H[2], o, sx, i, g.n[0], g.d[0], g.rd[0], p[0], p[1]);
+        cz = cz + bwd_diff(H[1], o, sx, i, g.n[0], g.d[0], g.rd[0], p[0], p[1]);
     }
     const uint8_t id = ids[o];
     const double ca = mats[id].ca, cb = mats[id].cb;

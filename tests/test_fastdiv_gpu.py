@@ -11,6 +11,10 @@ pytestmark = pytest.mark.gpu
 
 SPACINGS = [10e-6, 8e-6, 6e-6, 5e-6, 4e-6, 3e-6, 2e-6, 1e-6, 19e-6, 4e-6 / 3,
             1.0, 3.0, 0.1, 7.123456789e-5]
+# LLG divisors (llg.py:93-95,134): Ms values, 1 + |a|^2 just above 1 and
+# large, |M| near Ms -- ddiv with y = recip_of(d) replaces x / d there too
+LLG_DIVISORS = [9.7e5, 1.3926e5, 1.3926e5 * (1 + 2.0**-40), 1.0 + 2.0**-52, 1.0 + 1e-9,
+                1.0000123, 1.5, 2.0 - 2.0**-52, 37.25, 1e12, 1e150, 2.0**-500]
 
 
 def _samples(seed, n):
@@ -26,7 +30,7 @@ def _samples(seed, n):
     return np.concatenate([x, y, special])
 
 
-@pytest.mark.parametrize("d", SPACINGS)
+@pytest.mark.parametrize("d", SPACINGS + LLG_DIVISORS)
 def test_ddiv_matches_ieee_division(d):
     lib = _native.load_library()
     x = np.ascontiguousarray(_samples(hash(d) & 0xffff, 4_000_000))
