@@ -117,6 +117,33 @@ __global__ void k_div_selftest(const double* __restrict__ x, int64_t n, double d
     }
 }
 
+// The exact slow path of a batch of six divisions (guard failed: zeros,
+// subnormals, extreme exponents), out of line so the hot loop stays compact
+// in the instruction cache.  Divisors (dy, dy, dz, dz, dx, dx) as in both
+// curl batches.
+struct Q6 { double q0, q1, q2, q3, q4, q5; };
+
+// A failed batch guard is mostly exact zeros (fresh runs are zero almost
+// everywhere for thousands of steps).  For x = +-0 the fast-path value is a
+// zero of possibly the wrong sign, which cannot change any result: every
+// quotient enters the curl sums (em.py:130-138, 217-231) that start from
+// +0.0, and under round-to-nearest +0 + (+-0) and +0 - (+-0) are +0, so a
+// sum never holds -0 and the sign of a zero term never shows.  So a batch
+// whose failing numerators are all zeros keeps its fast-path quotients.
+__device__ __forceinline__ bool in_range_or_zero(double x) {
+    const unsigned u = ((unsigned)__double2hiint(x) << 1) - kGuardBias;
+    return u <= kGuardSpan || x == 0.0;
+}
+__device__ __noinline__ Q6 slow_div6(double a0, double a1, double a2, double a3, double a4,
+                                     double a5, double dx, double dy, double dz, double rx,
+                                     double ry, double rz) {
+    Q6 o;
+    o.q0 = xdiv(a0, dy, ry); o.q1 = xdiv(a1, dy, ry);
+    o.q2 = xdiv(a2, dz, rz); o.q3 = xdiv(a3, dz, rz);
+    o.q4 = xdiv(a4, dx, rx); o.q5 = xdiv(a5, dx, rx);
+    return o;
+}
+
 // H^{n+1} at one entry of the staged plane (in place in shared memory).
 // Straight-line: all six differences and divisions are issued back to back
 // and the division guard is checked once for the batch.
@@ -153,9 +180,14 @@ __device__ __forceinline__ void h_entry(const Geom& g, const HCtx& c, int e, int
     const bool bad = !g_fastdiv || (vx && gX > kGuardSpan) || (vy && gY > kGuardSpan) ||
                      (vz && gZ > kGuardSpan);
     if (__builtin_expect(bad, 0)) {
-        q0 = xdiv(a0, g.d[1], ry); q1 = xdiv(a1, g.d[1], ry);
-        q2 = xdiv(a2, g.d[2], rz); q3 = xdiv(a3, g.d[2], rz);
-        q4 = xdiv(a4, g.d[0], rx); q5 = xdiv(a5, g.d[0], rx);
+        bool fine = g_fastdiv;
+        if (vx) fine = fine && in_range_or_zero(a0) && in_range_or_zero(a2);
+        if (vy) fine = fine && in_range_or_zero(a3) && in_range_or_zero(a4);
+        if (vz) fine = fine && in_range_or_zero(a1) && in_range_or_zero(a5);
+        if (!fine) {
+            const Q6 o = slow_div6(a0, a1, a2, a3, a4, a5, g.d[0], g.d[1], g.d[2], rx, ry, rz);
+            q0 = o.q0; q1 = o.q1; q2 = o.q2; q3 = o.q3; q4 = o.q4; q5 = o.q5;
+        }
     }
     // em.py:130-138 accumulation order, collapsed axes omitted
     cx = 0.0; cy = 0.0; cz = 0.0;
@@ -339,9 +371,15 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
                     double q2 = qdiv(b2, g.d[2], rz, gg2), q3 = qdiv(b3, g.d[2], rz, gg2);
                     double q4 = qdiv(b4, g.d[0], rx, gg2), q5 = qdiv(b5, g.d[0], rx, gg2);
                     if (__builtin_expect(!fastdiv || gg2 > kGuardSpan, 0)) {
-                        q0 = xdiv(b0, g.d[1], ry); q1 = xdiv(b1, g.d[1], ry);
-                        q2 = xdiv(b2, g.d[2], rz); q3 = xdiv(b3, g.d[2], rz);
-                        q4 = xdiv(b4, g.d[0], rx); q5 = xdiv(b5, g.d[0], rx);
+                        const bool fine = fastdiv && in_range_or_zero(b0) &&
+                                          in_range_or_zero(b1) && in_range_or_zero(b2) &&
+                                          in_range_or_zero(b3) && in_range_or_zero(b4) &&
+                                          in_range_or_zero(b5);
+                        if (!fine) {
+                            const Q6 o = slow_div6(b0, b1, b2, b3, b4, b5, g.d[0], g.d[1],
+                                                   g.d[2], rx, ry, rz);
+                            q0 = o.q0; q1 = o.q1; q2 = o.q2; q3 = o.q3; q4 = o.q4; q5 = o.q5;
+                        }
                     }
                     double cx = 0.0, cy = 0.0, cz = 0.0;   // em.py:217-231 order
                     if (ay) { cx = cx + q0; cz = cz - q1; }
