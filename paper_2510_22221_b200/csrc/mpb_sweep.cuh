@@ -443,7 +443,7 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
 // curl E, H^n, M^n) and writes H^{n+1}, M^{n+1}; per-block residual history and
 // local-stop range feed the global stop rule (k_llg_fixup / all-reduce).
 // Ghost-plane copies (slabs) are computed for their H only.
-__global__ void __launch_bounds__(256) k_llg_local(Geom g, Bufs b,
+__global__ void __launch_bounds__(256, 3) k_llg_local(Geom g, Bufs b,
                                                    const mpb_material* __restrict__ mats,
                                                    const uint8_t* __restrict__ ids,
                                                    const int2* __restrict__ cells,
