@@ -77,7 +77,7 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
     }
     if (const char* e = getenv("MPB_SWEEP_V")) {
         const int v = atoi(e);
-        if (v == 1 || v == 2 || v == 4) fs->V = v;
+        if (v == 1 || v == 2) fs->V = v;
         if (fs->V != 2) fs->NT = kSweepThreads;
     }
     if (const char* e = getenv("MPB_SWEEP_NT"))
@@ -124,11 +124,9 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
     if (fs->NT == 256)
         rc = set_smem_attr<2, true, 256>(fs->smem);
     else if (fs->F3)
-        rc = fs->V == 4 ? set_smem_attr<4, true>(fs->smem)
-                        : (fs->V == 2 ? set_smem_attr<2, true>(fs->smem) : set_smem_attr<1, true>(fs->smem));
+        rc = fs->V == 2 ? set_smem_attr<2, true>(fs->smem) : set_smem_attr<1, true>(fs->smem);
     else
-        rc = fs->V == 4 ? set_smem_attr<4, false>(fs->smem)
-                        : (fs->V == 2 ? set_smem_attr<2, false>(fs->smem) : set_smem_attr<1, false>(fs->smem));
+        rc = fs->V == 2 ? set_smem_attr<2, false>(fs->smem) : set_smem_attr<1, false>(fs->smem);
     if (rc) return rc;
     {   // reciprocals of the spacings, computed once on the device
         for (int a = 0; a < 3; ++a) sc.rd[a] = g.rd[a];   // set in mpb_create
@@ -239,12 +237,10 @@ int launch_fused(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s, in
         k_sweep<2, true, 256><<<grid, 256, fs->smem, s>>>(g, b, h->mats, ids_view(h), h->st,
                                                          sc);
     } else if (fs->F3) {
-        if (fs->V == 4) MPB_LAUNCH(4, true);
-        else if (fs->V == 2) MPB_LAUNCH(2, true);
+        if (fs->V == 2) MPB_LAUNCH(2, true);
         else MPB_LAUNCH(1, true);
     } else {
-        if (fs->V == 4) MPB_LAUNCH(4, false);
-        else if (fs->V == 2) MPB_LAUNCH(2, false);
+        if (fs->V == 2) MPB_LAUNCH(2, false);
         else MPB_LAUNCH(1, false);
     }
 #undef MPB_LAUNCH
