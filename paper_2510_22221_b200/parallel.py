@@ -144,10 +144,12 @@ def slab_device_runs(config, materials, keys, slabs, device=0, **kw):
     return runs
 
 
-def run_group(config, nranks: int, bias=None, device: int = 0):
+def run_group(config, nranks: int, bias=None, device: int = 0, state=None, start: int = 0):
     """Run ``config`` as an ``nranks``-slab decomposition emulated on one GPU
     (mpb_group_run).  Returns (fields dict, M, probes dict, iterations) in
-    the global layout -- must equal sim.run bit for bit."""
+    the global layout -- must equal sim.run bit for bit.  ``state`` (global
+    E/H fields and M) with ``start`` continues from a mid-run state; the
+    probes and iterations returned then cover steps [start, n_steps)."""
     import ctypes as C
 
     from . import _native as N
@@ -161,13 +163,15 @@ def run_group(config, nranks: int, bias=None, device: int = 0):
     runs = slab_device_runs(config, materials, keys, slabs, device=device)
     try:
         fs = config.grid.field_shape
-        zeros = np.zeros(fs)
-        M0 = initial_magnetization(materials)
+        names = ("Ex", "Ey", "Ez", "Hx", "Hy", "Hz")
+        if state is None:
+            zeros = np.zeros(fs)
+            state = dict({n: zeros for n in names}, M=initial_magnetization(materials))
         for r, sl in zip(runs, slabs):
-            r.load_state({n: local_fields(sl, zeros) for n in
-                          ("Ex", "Ey", "Ez", "Hx", "Hy", "Hz")}, local_cells(sl, M0, axis=1))
-        steps = config.n_steps
-        src = source_values(config.source, config.dt, 0, steps)
+            r.load_state({n: local_fields(sl, state[n]) for n in names},
+                         local_cells(sl, state["M"], axis=1))
+        steps = config.n_steps - start
+        src = source_values(config.source, config.dt, start, config.n_steps)
         probes = [np.zeros((steps, max(1, len(keys)))) for _ in runs]
         iters = np.zeros(steps, dtype=np.int32)
         hs = (C.c_void_p * nranks)(*[r.h for r in runs])
@@ -175,7 +179,7 @@ def run_group(config, nranks: int, bias=None, device: int = 0):
             *[p.ctypes.data_as(C.POINTER(C.c_double)) for p in probes])
         fail = N.Failure()
         code = N.load_library().mpb_group_run(
-            hs, nranks, 0, steps, src.ctypes.data_as(C.POINTER(C.c_double)), pp,
+            hs, nranks, start, steps, src.ctypes.data_as(C.POINTER(C.c_double)), pp,
             iters.ctypes.data_as(C.POINTER(C.c_int32)), C.byref(fail))
         if code == N.ESTEP:
             return None, None, None, (int(fail.step), float(fail.residual),

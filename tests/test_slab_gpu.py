@@ -43,3 +43,37 @@ def test_slab_overlapped_exchange_matches_golden(name, nranks, overlap, monkeypa
     monkeypatch.setenv("MPB_SWEEP_MINCHUNK", "2")
     monkeypatch.setenv("MPB_OVERLAP", overlap)
     test_slab_group_matches_reference_golden(name, nranks)
+
+
+# Benchmark-size geometries in slabs: C2 (CPW + film, the C4 geometry family)
+# and C3 (7% magnetic film) from a mid-run state, 3 and 4 slabs with many
+# x-chunks each (interior/edge split of the overlapped exchange) against the
+# single-GPU run of the same state (itself bit-identical to the oracle,
+# tests/test_configs_gpu.py).
+@pytest.mark.parametrize("name,nranks,steps", [("c2", 3, 6), ("c3", 4, 4)])
+def test_slab_group_benchmark_geometry(name, nranks, steps):
+    from dataclasses import replace
+    from pathlib import Path
+
+    from paper_2510_22221_b200 import sim
+    from paper_2510_22221_b200.config import load_config
+    from tests.test_configs_gpu import mid_run_state
+
+    cfg = load_config(Path(__file__).resolve().parents[1] / "configs" / f"{name}.cfg")
+    start = 200
+    cfg = replace(cfg, t_end=(start + steps - 0.5) * cfg.dt)
+    state = mid_run_state(cfg, 11)
+    keys = list(dict.fromkeys((p[0], (p[1], p[2], p[3])) for p in cfg.probes))
+    snap = {"fields": {k: v.copy() for k, v in state.items()}, "step": start,
+            "probes": {k: np.zeros(start) for k in keys},
+            "iterations": np.ones(start, dtype=int)}
+    one = sim.run(cfg, resume=snap)
+    fields, M, probes, its = parallel.run_group(cfg, nranks, state=state, start=start)
+    assert fields is not None, its
+    st = one.lattice.state_arrays()
+    for k in ("Ex", "Ey", "Ez", "Hx", "Hy", "Hz"):
+        assert np.array_equal(fields[k], st[k]), k
+    assert np.array_equal(M, st["M"])
+    assert np.array_equal(its, one.iterations[start:])
+    for key in keys:
+        assert np.array_equal(probes[key], one.probes[key].samples[start:]), key
