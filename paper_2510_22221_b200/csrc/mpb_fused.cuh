@@ -83,8 +83,8 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
     if (const char* e = getenv("MPB_SWEEP_NT"))
         if (atoi(e) == 512) fs->NT = kSweepThreads;
     sc.T = fs->V * fs->NT;
-    if (const char* e = getenv("MPB_SWEEP_T")) {
-        const int t = atoi(e);
+    if (const char* e = getenv("MPB_SWEEP_T")) {   // even: 16-byte aligned tile starts
+        const int t = atoi(e) & ~1;
         if (t > 0 && t <= sc.T) sc.T = t;
     }
     sc.tiles = (g.FyFz + sc.T - 1) / sc.T;

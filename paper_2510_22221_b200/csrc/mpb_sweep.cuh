@@ -58,6 +58,22 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
+// shared -> global bulk copy (async proxy), tracked by bulk groups
+__device__ __forceinline__ void tma_store_1d(void* gdst, const void* ssrc, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+                 "r"(smem_u32(ssrc)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+// all but the newest bulk group have finished reading shared memory
+__device__ __forceinline__ void bulk_wait_read_all_but_1() {
+    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred P1;\n\tLAB_WAIT:\n\t"
@@ -234,6 +250,7 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
     const uint32_t ebytes = (uint32_t)(ae - a0) * 8u;
     const uint32_t hbytes = (uint32_t)(ah - a0) * 8u;
     const uint32_t ibytes = (uint32_t)(iae - ia0);
+    const uint32_t hst_bytes = (uint32_t)(((f1 + 1) & ~1) - f0) * 8u;   // 16-byte multiple
 
     for (int q = tid; q < sc.nmat; q += blockDim.x) {
         s_cacb[2 * q] = mats[q].ca;
@@ -275,6 +292,10 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
     // gives low thread ids the extra (halo) entries, so the last warp has
     // slack to absorb the issue time before the plane barrier
     constexpr int kIssuer = NT - 32;
+    // H^{n+1} written by bulk stores from the slot (two-CTA 256-thread form:
+    // +3-4% on C4); the one-CTA forms keep per-entry stores -- there the
+    // issuing warp's wait for the previous plane's stores stalls the whole SM
+    constexpr bool kBulkH = NT == 256;
     if (tid == kIssuer)
         for (int p = pstart; p <= plast && p < pstart + kSlots; ++p) issue(p);
 
@@ -328,9 +349,24 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
         // H^{n+1}(p) complete everywhere, and every thread is past E(p-1) and
         // H(p), the last readers of plane p-1's slot: refill it with p+2
         __syncthreads();
-        if (tid == kIssuer && p > pstart && p + 2 <= plast) {
-            fence_proxy_async();
-            issue(p + 2);
+        if (tid == kIssuer) {
+            fence_proxy_async();   // the H updates above -> async proxy
+            if constexpr (kBulkH) {
+                // H^{n+1} of the owned range leaves straight from the slot:
+                // three bulk stores instead of a store per entry and component
+                // (padding entries carry their staged zeros); the ghost plane
+                // of a slab is written too (k_edefer reads it pre-exchange)
+                if (p >= i0 || p == g.c0 - 1) {
+                    const int64_t pb = (int64_t)p * g.PP;
+                    for (int c = 0; c < 3; ++c)
+                        tma_store_1d(b.Hb[c] + pb + f0, sH(s, c) + (f0 - a0), hst_bytes);
+                }
+                bulk_commit();
+            }
+            if (p > pstart && p + 2 <= plast) {
+                if constexpr (kBulkH) bulk_wait_read_all_but_1();   // p-1's stores left its slot
+                issue(p + 2);
+            }
         }
 
         // ---- E^{n+1}(p, f) for the owned range ------------------------------
@@ -416,11 +452,13 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
                         if (zx) b.Eb[0][o + 1] = z1pec ? 0.0 : exa + kk * (w0 - Ex[e + 1]);
                         if (zy) b.Eb[1][o + 1] = z1pec ? 0.0 : eya + kk * (w1 - Ey[e + 1]);
                     }
-                    const bool cp = p < nx || !ax;
-                    if (j < ny && k < nz) b.Hb[0][o] = hx;
-                    if (cp && k < nz) b.Hb[1][o] = hy;
-                    if (cp && j < ny) b.Hb[2][o] = hz;
-                } else if (p == g.c0 - 1) {
+                    if constexpr (!kBulkH) {
+                        const bool cp = p < nx || !ax;
+                        if (j < ny && k < nz) b.Hb[0][o] = hx;
+                        if (cp && k < nz) b.Hb[1][o] = hy;
+                        if (cp && j < ny) b.Hb[2][o] = hz;
+                    }
+                } else if (!kBulkH && p == g.c0 - 1) {
                     // low ghost plane of a slab: its H^{n+1} is read by k_edefer
                     // (x-backward difference at plane c0) before the exchange
                     // delivers the owner's copy (identical values)
@@ -436,6 +474,7 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
             }
         }
     }
+    if (kBulkH && tid == kIssuer) bulk_wait_all();   // slots live until the stores read them
 }
 
 // LLG of the magnetic cells after the (pure Maxwell) sweep: each cell runs

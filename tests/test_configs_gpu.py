@@ -96,7 +96,7 @@ def test_config_geometry_matches_oracle(name, steps):
 @pytest.mark.parametrize("env", [
     {"MPB_SWEEP_NT": "512"},                       # V=2, one 512-thread CTA per SM (C5 form)
     {"MPB_SWEEP_V": "1"},                          # one entry per thread
-    {"MPB_SWEEP_T": "333", "MPB_SWEEP_MINCHUNK": "3"},   # ragged tiles and chunks
+    {"MPB_SWEEP_T": "334", "MPB_SWEEP_MINCHUNK": "3"},   # ragged tiles and chunks
 ])
 def test_sweep_tile_forms_match_oracle(env, monkeypatch):
     for k, v in env.items():
