@@ -219,3 +219,32 @@ def test_snapshot_resume_is_bit_identical(tmp_path):
     assert np.array_equal(resumed.iterations, full.iterations)
     for name, arr in full.lattice.state_arrays().items():
         assert np.array_equal(resumed.lattice.state_arrays()[name], arr)
+
+
+def test_closed_box_energy_bounded_3d_long_run():
+    """3D counterpart of the closed-box check (reference test_em.py:99-113):
+    a vacuum PEC box at 0.99 CFL, pulse injected then switched off, 20,000
+    steps; the on-device total_energy must neither drift (< 1e-3) nor
+    oscillate beyond 5% -- long-run stability of the fused 3D sweep."""
+    grid = GridSpec(24, 20, 28, 1e-6, 1.2e-6, 0.9e-6)
+    mm = MaterialMap(grid.cell_shape, MaterialCell()).freeze()
+    dt = em.cfl_timestep(grid, 0.99)
+    cfg = sim.SimConfig(grid=grid, materials=mm,
+                        source=em.SourceSpec(f0=150e9, Tp=0.5e-12, amplitude=1.0,
+                                             location=(7, 9, 11), polarization=(0, 1, 0)),
+                        boundaries=em.BoundarySpec(), cfl_factor=0.99,
+                        t_end=0.5 * dt, probes=())
+    st = Stepper(cfg)
+    try:
+        st.advance(1500)
+        energies = []
+        for _ in range(185):
+            st.advance(100, source_on=False)
+            energies.append(st.energy())
+    finally:
+        st.close()
+    e = np.asarray(energies)
+    assert e.min() > 0
+    drift = abs(e[-10:].mean() - e[:10].mean()) / e[:10].mean()
+    assert drift < 1e-3
+    assert e.max() / e.min() < 1.05
