@@ -102,3 +102,13 @@ def test_gpu_c1_64cubed_against_oracle(amp):
     assert np.array_equal(res.iterations, ref["iterations"])
     for key, v in ref["probes"].items():
         assert np.array_equal(res.probes[key].samples, v), key
+
+
+# z walls as separate launches instead of inside the sweep (MPB_ZWALL=kernel):
+# the other documented order of the same wall arithmetic, same bits
+@pytest.mark.parametrize("name", ["mixed3d", "allmur3d", "zwall_magnet", "pec_block"])
+def test_gpu_zwall_kernel_order_matches_golden(name, monkeypatch):
+    monkeypatch.setenv("MPB_ZWALL", "kernel")
+    case = CASES[name]
+    res = sim.run(build(case, mirror_namespace()), bias=case.get("bias"))
+    _assert_same(res, load(name))
