@@ -102,3 +102,25 @@ def test_sweep_tile_forms_match_oracle(env, monkeypatch):
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     _check("c2", 6)
+
+
+def test_nonzero_m_outside_magnets_is_preserved():
+    """A resumed state may carry M in non-magnetic cells (the reference never
+    touches it there); the library keeps such planes on the host and must hand
+    them back unchanged, bit for bit with the oracle."""
+    cfg = load_config(ROOT / "configs" / "c2.cfg")
+    start, steps = 50, 3
+    cfg = replace(cfg, t_end=(start + steps - 0.5) * cfg.dt)
+    state = mid_run_state(cfg, 3)
+    rng = np.random.default_rng(5)
+    mag = np.asarray(cfg.materials.Ms) > 0
+    state["M"] = np.where(mag, state["M"], rng.standard_normal(state["M"].shape))
+    keys = [(p[0], (p[1], p[2], p[3])) for p in cfg.probes]
+    snap = {"fields": state, "step": start, "probes": {k: np.zeros(start) for k in keys},
+            "iterations": np.ones(start, dtype=int)}
+    ref = orc.run(cfg, resume={**snap, "fields": {k: v.copy() for k, v in state.items()}})
+    res = sim.run(cfg, resume=snap)
+    for k, v in ref["fields"].items():
+        assert np.array_equal(res.lattice.state_arrays()[k], v), k
+    for key, v in ref["probes"].items():
+        assert np.array_equal(res.probes[key].samples, v), key
