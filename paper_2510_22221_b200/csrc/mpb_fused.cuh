@@ -98,7 +98,6 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
     sc.hcap = (sc.T + sc.hl + 4 + 1) & ~1;
     sc.icap = sc.T + sc.hl + 48;
     sc.stage_bytes = ((3 * sc.ecap + 3 * sc.hcap) * 8 + sc.icap + 127) / 128 * 128;
-    sc.ring_offset = 0;
     fs->smem = (size_t)kSlots * sc.stage_bytes;
 
     const size_t static_smem = 8 * 1024;

@@ -98,7 +98,6 @@ struct SweepCfg {
     int icap;           // bytes of ids per slot
     uint32_t fz_magic;  // j = umulhi(f, magic) for f < FyFz
     int stage_bytes;    // bytes per ring slot
-    int ring_offset;    // bytes of dynamic smem before the ring (0)
     int ch_base;        // chunk of blockIdx.x / tiles == 0 (launch subsets)
     int ch_step;        // chunk stride between consecutive block rows
     int nmat;           // entries of the material table
@@ -222,7 +221,7 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
     __shared__ double s_cacb[MPB_MAX_MATERIALS * 2];
 
     __shared__ double s_murz[MPB_MAX_MATERIALS];
-    unsigned char* ring = smem + sc.ring_offset;
+    unsigned char* ring = smem;
 
     if (st->fail) return;
     const int tid = threadIdx.x;
