@@ -19,6 +19,7 @@
 #include "mpb_device.cuh"
 #include "mpb_kernels_split.cuh"
 #include "mpb_sweep.cuh"
+#include "mpb_line.cuh"
 
 using namespace mpb;
 
@@ -107,6 +108,10 @@ struct mpb_handle {
     // exchange runs on comm_stream after ev_post, the edge chunks wait ev_exch
     bool overlap = false;
     bool exch_pending = false;
+    // lines along z: the whole run in one shared-memory-resident CTA (mpb_line.cuh)
+    bool line = false;
+    size_t line_smem = 0;
+    LineProbe* lprobes = nullptr;
     cudaStream_t comm_stream = nullptr;
     cudaEvent_t ev_post = nullptr, ev_exch = nullptr;
     // host copy of M on the local cell planes (cells outside the device M
@@ -494,7 +499,10 @@ int64_t launches_per_step(mpb_handle* h) {
 }
 
 // Enqueue nsteps steps; buffers already pointed to by the device state.
+int launch_line(mpb_handle* h, int64_t nsteps);
+
 int enqueue_steps(mpb_handle* h, int64_t nsteps) {
+    if (h->line) return launch_line(h, nsteps);
     int64_t s = 0;
     const bool use_graph = !h->timing && h->graph_steps > 1;
     while (s < nsteps) {
@@ -578,6 +586,46 @@ int upload_probes(mpb_handle* h) {
     }
     CU(cudaMemcpy(h->probes, pd.data(), sizeof(ProbeDesc) * pd.size(),
                   cudaMemcpyHostToDevice));
+    if (h->line) {   // the same probes, addressed in the line kernel's shared state
+        std::vector<LineProbe> lp((size_t)std::max(1, h->nprobes));
+        for (int p = 0; p < h->nprobes; ++p) {
+            const int comp = h->probe_comp[p];
+            const int k = h->probe_loc[3 * p + 2];
+            LineProbe q{};
+            if (comp < MPB_COMP_MX || h->mplanes) { q.src = comp; q.idx = k; }
+            else { q.src = -1; q.constant = pd[(size_t)p].constant; }
+            lp[(size_t)p] = q;
+        }
+        CU(cudaMemcpy(h->lprobes, lp.data(), sizeof(LineProbe) * lp.size(),
+                      cudaMemcpyHostToDevice));
+    }
+    return MPB_OK;
+}
+
+// The whole of nsteps in one launch of the line kernel (mpb_line.cuh).
+int launch_line(mpb_handle* h, int64_t nsteps) {
+    if (nsteps <= 0) return MPB_OK;
+    const int pa = h->parity, pb = (int)((h->parity + nsteps) & 1);
+    LineArgs a{};
+    for (int c = 0; c < 3; ++c) {
+        a.E[c] = h->E[pa][c]; a.H[c] = h->H[pa][c]; a.M[c] = h->mplanes ? h->M[pa][c] : nullptr;
+        a.Eo[c] = h->E[pb][c]; a.Ho[c] = h->H[pb][c]; a.Mo[c] = h->mplanes ? h->M[pb][c] : nullptr;
+        a.src_pol[c] = h->src.pol[c];
+    }
+    a.ids = h->ids;
+    a.mats = h->mats;
+    a.magcells = h->magcells;
+    a.nmag = h->nmag;
+    a.nmat = h->nmat_table;
+    a.probes = h->lprobes;
+    a.nprobes = h->nprobes;
+    a.src_off = (int)h->src.off;
+    a.any_magnetic = h->any_magnetic;
+    a.nsteps = (int)nsteps;
+    k_line<<<1, kLineThreads, h->line_smem, h->stream>>>(h->g, a, h->st);
+    CU(cudaGetLastError());
+    h->parity = pb;
+    h->launches_last += 1;
     return MPB_OK;
 }
 
@@ -790,6 +838,22 @@ int mpb_create(const mpb_setup* su, mpb_handle** out) {
         rc = prepare_fused(h, g);
         if (rc) { mpb_destroy(h); return rc; }
     }
+    {   // lines along z that fit in one CTA's shared memory run in k_line
+        const char* e = getenv("MPB_LINE");
+        const bool want = !(e && atoi(e) == 0);
+        const size_t need = ((size_t)9 * g.F[2] + 3 * (size_t)h->nmat_table) * sizeof(double) +
+                            (size_t)g.F[2] + 16;
+        int optin = 0;
+        CU(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
+        if (want && h->nranks == 1 && h->variant == 0 && g.n[0] == 1 && g.n[1] == 1 &&
+            g.act[2] && g.n[2] >= 2 && h->nmag <= kLineThreads &&
+            need + 1024 <= (size_t)optin) {
+            h->line = true;
+            h->line_smem = need;
+            CU(cudaFuncSetAttribute(k_line, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)need));
+        }
+    }
 
     // source (em.py:276-282): only the owning rank injects
     for (int a = 0; a < 3; ++a) {
@@ -819,6 +883,7 @@ int mpb_create(const mpb_setup* su, mpb_handle** out) {
             }
     }
     chk(dev_alloc(h, &h->probes, (size_t)std::max(1, h->nprobes)));
+    if (h->line) chk(dev_alloc(h, &h->lprobes, (size_t)std::max(1, h->nprobes)));
     h->hostM.clear();
     if (rc) { mpb_destroy(h); return rc; }
     bool zero_id = true;
@@ -843,6 +908,7 @@ void mpb_destroy(mpb_handle* h) {
     cudaSetDevice(h->device);
     if (h->stream) cudaStreamSynchronize(h->stream);
     for (auto& e : h->events) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+    cudaFree(h->lprobes);
     for (int p = 0; p < 2; ++p) {
         if (h->graph[p]) cudaGraphExecDestroy(h->graph[p]);
         for (int c = 0; c < 3; ++c) {
