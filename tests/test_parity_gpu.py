@@ -112,3 +112,23 @@ def test_gpu_zwall_kernel_order_matches_golden(name, monkeypatch):
     case = CASES[name]
     res = sim.run(build(case, mirror_namespace()), bias=case.get("bias"))
     _assert_same(res, load(name))
+
+
+# Lines along z run in the shared-memory line kernel by default (k_line);
+# the general kernels must still give the same bits for them (MPB_LINE=0),
+# including the StepFailure case.
+@pytest.mark.parametrize("name", ["cavity1d", "small1d_strong"])
+def test_gpu_line_general_path_matches_golden(name, monkeypatch):
+    monkeypatch.setenv("MPB_LINE", "0")
+    case = CASES[name]
+    _assert_same(sim.run(build(case, mirror_namespace()), bias=case.get("bias")), load(name))
+
+
+def test_gpu_line_general_path_step_failure(monkeypatch):
+    monkeypatch.setenv("MPB_LINE", "0")
+    g = load("fail_tol")
+    cfg = build(CASES["fail_tol"], mirror_namespace())
+    with pytest.raises(llg.StepFailure) as ei:
+        sim.run(cfg)
+    assert ei.value.step == int(g["fail_step"])
+    assert str(ei.value) == str(g["fail_message"])
