@@ -1,9 +1,10 @@
 // mpb_sweep.cuh -- the fused coupled-step sweep for sm_100a.
 //
-// One kernel computes, per entry, H^{n+1} (plain update or the cell's LLG
-// fixed point to its local stop) and E^{n+1} in a single pass over the
-// lattice, so each of the 6 field arrays is read once and written once per
-// step (96 B/cell in fp64, the roofline numerator of SURVEY 8d).
+// One kernel computes, per entry, the plain H^{n+1} (magnetic cells too; the
+// LLG of the few magnetic cells runs afterwards in k_llg_local / k_edefer) and
+// E^{n+1} in a single pass over the lattice, so each of the 6 field arrays is
+// read once and written once per step (96 B/cell in fp64, the roofline
+// numerator of SURVEY 8d).
 //
 // Decomposition: each CTA owns a contiguous range [f0,f1) of T entries of an
 // x-plane (a few z-rows; z is contiguous) and a chunk [i0,i1) of planes, and
@@ -16,8 +17,10 @@
 // j-1 halo row, recomputed rather than exchanged), then E^{n+1} of the owned
 // range is formed from it plus the previous plane's Hy, Hz kept in registers
 // (the x-backward difference), so no x-halo is ever re-read from HBM except
-// one plane per chunk.  Reads come from one ping-pong buffer set and writes
-// go to the other, so CTAs never race on halos.
+// one plane per chunk.  One CTA barrier per plane (between the H and E
+// phases); every thread waits on the slot's mbarrier itself.  Reads come from
+// one ping-pong buffer set and writes go to the other, so CTAs never race on
+// halos.
 //
 // Exactness: same operation order as the split kernels / the reference
 // (em.py:117-139, 171-182, 206-272; llg.py:108-148); divisions by dx,dy,dz use
