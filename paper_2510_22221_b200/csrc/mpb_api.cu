@@ -168,13 +168,21 @@ Bufs make_bufs(const mpb_handle* h, int pa) {
 
 const uint8_t* ids_view(const mpb_handle* h) { return view(h->ids, h); }
 
+// Stream-ordered allocations on the handle's stream: neither allocating nor
+// freeing a handle synchronises the device, so concurrent runs on one GPU
+// (bias sweeps) do not stall each other's kernels.
 template <typename T>
 int dev_alloc(mpb_handle* h, T** p, size_t count) {
     if (count == 0) { *p = nullptr; return MPB_OK; }
-    CU(cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T)));
-    CU(cudaMemset(*p, 0, count * sizeof(T)));
+    CU(cudaMallocAsync(reinterpret_cast<void**>(p), count * sizeof(T), h->stream));
+    CU(cudaMemsetAsync(*p, 0, count * sizeof(T), h->stream));
+    CU(cudaStreamSynchronize(h->stream));   // ready for synchronous copies
     h->bytes += (int64_t)(count * sizeof(T));
     return MPB_OK;
+}
+
+void dev_free(mpb_handle* h, void* p) {
+    if (p) cudaFreeAsync(p, h->stream);
 }
 
 int reset_state(mpb_handle* h) {
@@ -828,11 +836,12 @@ int mpb_create(const mpb_setup* su, mpb_handle** out) {
     }
     {   // reciprocals of the spacings for the exact-division fast path
         double* dr = nullptr;
-        CU(cudaMalloc(&dr, 3 * sizeof(double)));
-        k_recips<<<1, 1>>>(g.d[0], g.d[1], g.d[2], dr);
+        CU(cudaMallocAsync(&dr, 3 * sizeof(double), h->stream));
+        k_recips<<<1, 1, 0, h->stream>>>(g.d[0], g.d[1], g.d[2], dr);
         CU(cudaGetLastError());
-        CU(cudaMemcpy(g.rd, dr, 3 * sizeof(double), cudaMemcpyDeviceToHost));
-        cudaFree(dr);
+        CU(cudaMemcpyAsync(g.rd, dr, 3 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+        CU(cudaFreeAsync(dr, h->stream));
+        CU(cudaStreamSynchronize(h->stream));
     }
     if (h->variant != 1) {
         rc = prepare_fused(h, g);
@@ -908,26 +917,27 @@ void mpb_destroy(mpb_handle* h) {
     cudaSetDevice(h->device);
     if (h->stream) cudaStreamSynchronize(h->stream);
     for (auto& e : h->events) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
-    cudaFree(h->lprobes);
+    dev_free(h, h->lprobes);
     for (int p = 0; p < 2; ++p) {
         if (h->graph[p]) cudaGraphExecDestroy(h->graph[p]);
         for (int c = 0; c < 3; ++c) {
-            cudaFree(h->E[p][c]);
-            cudaFree(h->H[p][c]);
-            cudaFree(h->M[p][c]);
+            dev_free(h, h->E[p][c]);
+            dev_free(h, h->H[p][c]);
+            dev_free(h, h->M[p][c]);
         }
     }
-    cudaFree(h->ids);
-    cudaFree(h->mats);
-    cudaFree(h->magcells);
-    cudaFree(h->magowned);
-    cudaFree(h->scratch);
-    cudaFree(h->st);
-    cudaFree(h->probes);
-    cudaFree(h->d_src);
-    cudaFree(h->d_probe);
-    cudaFree(h->d_iters);
+    dev_free(h, h->ids);
+    dev_free(h, h->mats);
+    dev_free(h, h->magcells);
+    dev_free(h, h->magowned);
+    dev_free(h, h->scratch);
+    dev_free(h, h->st);
+    dev_free(h, h->probes);
+    dev_free(h, h->d_src);
+    dev_free(h, h->d_probe);
+    dev_free(h, h->d_iters);
     destroy_fused(h);
+    if (h->stream) cudaStreamSynchronize(h->stream);
     if (h->comm) ncclCommDestroy(h->comm);
     if (h->ev_post) cudaEventDestroy(h->ev_post);
     if (h->ev_exch) cudaEventDestroy(h->ev_exch);
@@ -1060,11 +1070,12 @@ int mpb_run(mpb_handle* h, int64_t n0, int64_t nsteps, const double* src_vals,
     CU(cudaSetDevice(h->device));
     const int64_t cap = std::min<int64_t>(std::max<int64_t>(nsteps, 1), kRunChunk);
     if (cap > h->stage_cap) {
-        cudaFree(h->d_src); cudaFree(h->d_probe); cudaFree(h->d_iters);
+        dev_free(h, h->d_src); dev_free(h, h->d_probe); dev_free(h, h->d_iters);
         h->d_src = nullptr; h->d_probe = nullptr; h->d_iters = nullptr;
-        CU(cudaMalloc(&h->d_src, cap * sizeof(double)));
-        CU(cudaMalloc(&h->d_probe, cap * std::max(1, h->nprobes) * sizeof(double)));
-        CU(cudaMalloc(&h->d_iters, cap * sizeof(int)));
+        CU(cudaMallocAsync(&h->d_src, cap * sizeof(double), h->stream));
+        CU(cudaMallocAsync(&h->d_probe, cap * std::max(1, h->nprobes) * sizeof(double),
+                           h->stream));
+        CU(cudaMallocAsync(&h->d_iters, cap * sizeof(int), h->stream));
         h->stage_cap = cap;
     }
     int64_t launches = 0;
@@ -1232,12 +1243,12 @@ int mpb_total_energy(mpb_handle* h, double* out) {
         Mm[c] = h->M[p][c];
     }
     const double** dptr = nullptr;
-    CU(cudaMalloc(&dptr, 9 * sizeof(double*)));
+    CU(cudaMallocAsync(&dptr, 9 * sizeof(double*), h->stream));
     const double* hp[9] = {E[0], E[1], E[2], Hh[0], Hh[1], Hh[2], Mm[0], Mm[1], Mm[2]};
-    CU(cudaMemcpy(dptr, hp, sizeof hp, cudaMemcpyHostToDevice));
+    CU(cudaMemcpyAsync(dptr, hp, sizeof hp, cudaMemcpyHostToDevice, h->stream));
     const int blocks = 1184;
     double* partial = nullptr;
-    CU(cudaMalloc(&partial, 3 * blocks * sizeof(double)));
+    CU(cudaMallocAsync(&partial, 3 * blocks * sizeof(double), h->stream));
     k_energy_partial<<<blocks, 256, 0, h->stream>>>(g, dptr, dptr + 3, dptr + 6, h->mats,
                                                     ids_view(h), partial);
     CU(cudaGetLastError());
@@ -1245,8 +1256,8 @@ int mpb_total_energy(mpb_handle* h, double* out) {
     CU(cudaMemcpyAsync(hpart.data(), partial, hpart.size() * sizeof(double),
                        cudaMemcpyDeviceToHost, h->stream));
     CU(cudaStreamSynchronize(h->stream));
-    cudaFree(partial);
-    cudaFree(dptr);
+    dev_free(h, partial);
+    dev_free(h, dptr);
     double se = 0.0, sh = 0.0, sm = 0.0;
     for (int b = 0; b < blocks; ++b) {
         se += hpart[3 * b];

@@ -155,7 +155,8 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
         for (size_t q = 0; q < keys.size(); ++q)
             list[q] = make_int2((int)(keys[q] / g.FyFz), (int)(keys[q] % g.FyFz));
         fs->ndefer = (int)list.size();
-        CU(cudaMalloc(&fs->defer, sizeof(int2) * list.size()));
+        CU(cudaMallocAsync(&fs->defer, sizeof(int2) * list.size(), h->stream));
+        CU(cudaStreamSynchronize(h->stream));
         h->bytes += (int64_t)(sizeof(int2) * list.size());
         CU(cudaMemcpy(fs->defer, list.data(), sizeof(int2) * list.size(),
                       cudaMemcpyHostToDevice));
@@ -174,7 +175,8 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
             for (int j = 0; j < g.F[1]; ++j) lines.push_back(make_int3(1, i, j));
         fs->nzlines = (int)lines.size();
         if (fs->nzlines) {
-            CU(cudaMalloc(&fs->zlines, sizeof(int3) * lines.size()));
+            CU(cudaMallocAsync(&fs->zlines, sizeof(int3) * lines.size(), h->stream));
+            CU(cudaStreamSynchronize(h->stream));
             h->bytes += (int64_t)(sizeof(int3) * lines.size());
             CU(cudaMemcpy(fs->zlines, lines.data(), sizeof(int3) * lines.size(),
                           cudaMemcpyHostToDevice));
@@ -206,8 +208,8 @@ int launch_llg_local(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s
 void destroy_fused(mpb_handle* h) {
     FusedState* fs = fused_of(h);
     if (!fs) return;
-    cudaFree(fs->defer);
-    cudaFree(fs->zlines);
+    if (fs->defer) cudaFreeAsync(fs->defer, h->stream);
+    if (fs->zlines) cudaFreeAsync(fs->zlines, h->stream);
     delete fs;
     h->fused = nullptr;
 }

@@ -15,6 +15,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field, replace
 
+import functools
+
 import numpy as np
 
 from . import em, llg
@@ -105,10 +107,16 @@ def _wrap_source(loc, shape):
     return tuple(out)
 
 
-def source_values(src: em.SourceSpec, dt: float, start: int, stop: int) -> np.ndarray:
-    """v((n+1) dt) for n in [start, stop) with the reference's Python math."""
+@functools.lru_cache(maxsize=16)
+def _source_values(src: em.SourceSpec, dt: float, start: int, stop: int) -> np.ndarray:
     return np.array([em.source_value(src, (n + 1) * dt) for n in range(start, stop)],
                     dtype=np.float64)
+
+
+def source_values(src: em.SourceSpec, dt: float, start: int, stop: int) -> np.ndarray:
+    """v((n+1) dt) for n in [start, stop) with the reference's Python math
+    (one Python call per step, so cached: the runs of a bias sweep share it)."""
+    return _source_values(src, float(dt), int(start), int(stop)).copy()
 
 
 def _device_run_args(config, keys) -> dict:
