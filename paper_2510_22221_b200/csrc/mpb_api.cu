@@ -74,7 +74,10 @@ struct mpb_handle {
     int nranks = 1, rank = 0;
     int lo = 0, hi = 1, clo = 0, chi = 1;
     int any_magnetic = 0;
-    ncclComm_t comm = nullptr;
+    ncclComm_t comm = nullptr;     // LLG all-reduces (library stream)
+    ncclComm_t comm_x = nullptr;   // boundary exchange (comm stream): its own
+                                   // communicator, so the two streams never
+                                   // share one concurrently
     int64_t nloc = 0;              // (hi - lo) * PP
     int64_t mplanes = 0;           // mx1 - mx0
     double* E[2][3] = {};          // allocations (local planes)
@@ -205,25 +208,26 @@ int exchange(mpb_handle* h, int pb, cudaStream_t s) {
     auto plane = [&](double* alloc, int i) { return alloc + (int64_t)(i - h->lo) * g.PP; };
     auto mplane = [&](double* alloc, int i) { return alloc + (int64_t)(i - g.mx0) * g.PP; };
     auto has_m = [&](int i) { return h->mplanes > 0 && i >= g.mx0 && i < g.mx1; };
+    ncclComm_t xc = h->comm_x ? h->comm_x : h->comm;
     NC(ncclGroupStart());
     if (h->rank + 1 < h->nranks) {
         const int up = h->rank + 1;
         for (int c = 0; c < 3; ++c) {
-            NC(ncclSend(plane(h->E[pb][c], g.c1 - 1), n, ncclDouble, up, h->comm, s));
-            NC(ncclSend(plane(h->H[pb][c], g.c1 - 1), n, ncclDouble, up, h->comm, s));
+            NC(ncclSend(plane(h->E[pb][c], g.c1 - 1), n, ncclDouble, up, xc, s));
+            NC(ncclSend(plane(h->H[pb][c], g.c1 - 1), n, ncclDouble, up, xc, s));
             if (has_m(g.c1 - 1))
-                NC(ncclSend(mplane(h->M[pb][c], g.c1 - 1), n, ncclDouble, up, h->comm, s));
-            NC(ncclRecv(plane(h->E[pb][c], g.c1), n, ncclDouble, up, h->comm, s));
+                NC(ncclSend(mplane(h->M[pb][c], g.c1 - 1), n, ncclDouble, up, xc, s));
+            NC(ncclRecv(plane(h->E[pb][c], g.c1), n, ncclDouble, up, xc, s));
         }
     }
     if (h->rank > 0) {
         const int dn = h->rank - 1;
         for (int c = 0; c < 3; ++c) {
-            NC(ncclRecv(plane(h->E[pb][c], g.c0 - 1), n, ncclDouble, dn, h->comm, s));
-            NC(ncclRecv(plane(h->H[pb][c], g.c0 - 1), n, ncclDouble, dn, h->comm, s));
+            NC(ncclRecv(plane(h->E[pb][c], g.c0 - 1), n, ncclDouble, dn, xc, s));
+            NC(ncclRecv(plane(h->H[pb][c], g.c0 - 1), n, ncclDouble, dn, xc, s));
             if (has_m(g.c0 - 1))
-                NC(ncclRecv(mplane(h->M[pb][c], g.c0 - 1), n, ncclDouble, dn, h->comm, s));
-            NC(ncclSend(plane(h->E[pb][c], g.c0), n, ncclDouble, dn, h->comm, s));
+                NC(ncclRecv(mplane(h->M[pb][c], g.c0 - 1), n, ncclDouble, dn, xc, s));
+            NC(ncclSend(plane(h->E[pb][c], g.c0), n, ncclDouble, dn, xc, s));
         }
     }
     NC(ncclGroupEnd());
@@ -905,6 +909,13 @@ int mpb_create(const mpb_setup* su, mpb_handle** out) {
             mpb_destroy(h);
             return fail_msg(MPB_ECUDA, "ncclCommInitRank failed: %s", ncclGetErrorString(r));
         }
+        if (h->overlap) {   // collective over the ranks, same order everywhere
+            r = ncclCommSplit(h->comm, 0, h->rank, &h->comm_x, nullptr);
+            if (r != ncclSuccess) {
+                mpb_destroy(h);
+                return fail_msg(MPB_ECUDA, "ncclCommSplit failed: %s", ncclGetErrorString(r));
+            }
+        }
     }
     rc = reset_state(h);
     if (rc) { mpb_destroy(h); return rc; }
@@ -938,6 +949,7 @@ void mpb_destroy(mpb_handle* h) {
     dev_free(h, h->d_iters);
     destroy_fused(h);
     if (h->stream) cudaStreamSynchronize(h->stream);
+    if (h->comm_x) ncclCommDestroy(h->comm_x);
     if (h->comm) ncclCommDestroy(h->comm);
     if (h->ev_post) cudaEventDestroy(h->ev_post);
     if (h->ev_exch) cudaEventDestroy(h->ev_exch);
