@@ -148,6 +148,30 @@ CASES = {
         cfl=0.9, steps=200,
         probes=[("Ex", 1, 1, 1), ("Ey", 3, 0, 0), ("My", 2, 1, 1)],
     ),
+    # 1D along y (collapsed x, z): the sweep with one-entry rows (Fz = 1)
+    "yline1d": dict(
+        grid=(1, 50, 1, 3e-6, 3e-6, 3e-6),
+        background=(2e-4, 6.0),
+        boxes=[dict(box=(0, 1, 25, 26, 0, 1), sigma=1e-3, eps_r=1.0, Ms=9.7e5,
+                    alpha=0.003, bias=1700.0 * OE, bias_direction=(1, 0, 1))],
+        source=dict(f0=14.3e9, Tp=1e-12, amplitude=3e6, location=(0, 6, 0),
+                    polarization=(0.0, 0.0, 1.0)),
+        boundaries=dict(y0="MUR1", y1="PMC"),
+        cfl=0.95, steps=300,
+        probes=[("Ez", 0, 12, 0), ("Ex", 0, 30, 0), ("Mx", 0, 25, 0), ("Hy", 0, 24, 0)],
+    ),
+    # 2D in x-z (collapsed y): one-entry row halo, z walls with MUR1
+    "plane_xz": dict(
+        grid=(10, 1, 12, 5e-6, 5e-6, 4e-6),
+        background=(0.0, 2.5),
+        boxes=[dict(box=(4, 7, 0, 1, 5, 8), eps_r=15.0, Ms=1.3926e5, alpha=2e-3,
+                    bias=1200.0 * OE, bias_direction=(0, 1, 0))],
+        source=dict(f0=50e9, Tp=1e-12, amplitude=1e7, location=(2, 0, 3),
+                    polarization=(0.0, 1.0, 0.0)),
+        boundaries=dict(x0="PMC", x1="MUR1", z0="MUR1", z1="PEC"),
+        cfl=0.9, steps=150,
+        probes=[("Ey", 5, 0, 6), ("Hx", 5, 0, 6), ("My", 5, 0, 6), ("Ex", 0, 0, 0)],
+    ),
     # bias override through run(bias=...) along a tilted sweep direction
     "bias3d": dict(
         grid=(8, 9, 10, 6e-6, 6e-6, 6e-6),
