@@ -26,7 +26,11 @@ def digest(a) -> str:
     return hashlib.sha256(a.dtype.str.encode() + str(a.shape).encode() + a.tobytes()).hexdigest()
 
 
-def test_shipped_cavity_full_length_bitwise():
+# line kernel (default for z-lines) and the general kernels; either way the
+# 499,655 steps cross eight 65,536-step host staging chunks of mpb_run
+@pytest.mark.parametrize("line", ["1", "0"])
+def test_shipped_cavity_full_length_bitwise(line, monkeypatch):
+    monkeypatch.setenv("MPB_LINE", line)
     gold = json.loads((ROOT / "tests" / "golden" / "cavity1d_full.json").read_text())
     res = sim.run(load_config(ROOT / "configs" / "cavity1d.cfg"))
     assert res.steps == gold["steps"] == 499655
