@@ -118,7 +118,7 @@ def build_parser() -> argparse.ArgumentParser:
     p = argparse.ArgumentParser(prog="magphon-b200",
                                 description="B200 coupled Maxwell-LLG stepper")
     p.add_argument("--seed", type=int, default=0, help="accepted for compatibility")
-    p.add_argument("--parallel", type=int, default=1, help="GPUs used by sweeps")
+    p.add_argument("--parallel", type=int, default=1, help="concurrent sweep runs (spread over the GPUs, several per GPU)")
     p.add_argument("--dry-run", action="store_true")
     p.add_argument("--out", default=None, help="output directory ($MAGPHON_OUT or .)")
     sub = p.add_subparsers(dest="command", required=True)
