@@ -109,7 +109,11 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
     int waves = fs->NT == 256 ? 32 : 16;
     if (const char* e = getenv("MPB_SWEEP_WAVES")) waves = std::max(1, atoi(e));
     const int want = std::max(1, (waves * sms + sc.tiles - 1) / sc.tiles);
-    int minch = 8;   // >= 8 planes per chunk (pipeline fill is 3 planes)
+    // >= 8 planes per chunk (the pipeline fill is 3 planes), or >= 4 when
+    // 8-plane chunks would not even give two waves of CTAs (small grids,
+    // C1: +14%)
+    const int per_sm = fs->NT == 256 ? 2 : 1;
+    int minch = sc.tiles * (Fx / 8) < 2 * per_sm * sms ? 4 : 8;
     if (const char* e = getenv("MPB_SWEEP_MINCHUNK")) minch = std::max(2, atoi(e));
     const int maxch = std::max(1, Fx / minch);
     sc.nchunks = std::max(1, std::min(want, maxch));
