@@ -230,13 +230,22 @@ class DeviceRun:
         return out
 
     # -- stepping ------------------------------------------------------------
-    def run(self, n0: int, src_vals: np.ndarray):
+    def run(self, n0: int, src_vals: np.ndarray, probes: np.ndarray | None = None,
+            iters: np.ndarray | None = None):
         """Advance len(src_vals) steps.  Returns (probes[steps, P], iters,
-        failure) with failure None or (step, residual, iterations, kind)."""
+        failure) with failure None or (step, residual, iterations, kind).
+        ``probes`` / ``iters`` may be caller-provided (e.g. pinned) host
+        arrays of shape (steps, max(1, P)) float64 / (steps,) int32."""
         src = np.ascontiguousarray(src_vals, dtype=np.float64)
         steps = src.size
-        probes = np.zeros((steps, max(1, len(self.probes))))
-        iters = np.zeros(steps, dtype=np.int32)
+        if probes is None:
+            probes = np.zeros((steps, max(1, len(self.probes))))
+        if iters is None:
+            iters = np.zeros(steps, dtype=np.int32)
+        if (probes.shape != (steps, max(1, len(self.probes))) or probes.dtype != np.float64
+                or not probes.flags.c_contiguous or iters.shape != (steps,)
+                or iters.dtype != np.int32):
+            raise ValueError("probe / iteration buffers do not match the run")
         fail = N.Failure()
         code = self.lib.mpb_run(self.h, n0, steps,
                                 src.ctypes.data_as(C.POINTER(C.c_double)),
