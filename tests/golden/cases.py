@@ -172,6 +172,41 @@ CASES = {
         cfl=0.9, steps=150,
         probes=[("Ey", 5, 0, 6), ("Hx", 5, 0, 6), ("My", 5, 0, 6), ("Ex", 0, 0, 0)],
     ),
+    # the benchmark geometry in miniature: CPW strip + grounds as 1e11 S/m
+    # boxes on a Si substrate, YIG film on the strip, all-MUR1 walls
+    "cpw_small": dict(
+        grid=(20, 24, 16, 10e-6, 10e-6, 2e-6),
+        background=(0.0, 1.0),
+        boxes=[dict(box=(0, 20, 0, 24, 0, 6), eps_r=11.4),
+               dict(box=(0, 20, 0, 9, 6, 7), sigma=1e11),
+               dict(box=(0, 20, 15, 24, 6, 7), sigma=1e11),
+               dict(box=(0, 20, 11, 13, 6, 7), sigma=1e11),
+               dict(box=(5, 15, 11, 13, 7, 9), eps_r=15.0, Ms=1.3926e5, alpha=1e-3,
+                    bias=1000.0 * OE, bias_direction=(1, 0, 0))],
+        source=dict(f0=60e9, Tp=0.5e-12, amplitude=1e8, location=(3, 10, 6),
+                    polarization=(0.0, 1.0, 0.0)),
+        boundaries=dict(x0="MUR1", x1="MUR1", y0="MUR1", y1="MUR1", z0="MUR1",
+                        z1="MUR1"),
+        cfl=0.9, steps=150,
+        probes=[("Ey", 3, 10, 6), ("Ex", 10, 12, 7), ("Mz", 10, 12, 8), ("Hy", 10, 12, 8)],
+    ),
+    # two magnets of different materials and bias directions, conductor
+    # between them, mixed walls, very strong drive
+    "two_magnets": dict(
+        grid=(14, 12, 10, 6e-6, 5e-6, 4e-6),
+        background=(1e-3, 2.0),
+        boxes=[dict(box=(2, 5, 3, 7, 2, 6), eps_r=15.0, Ms=9.7e5, alpha=3e-3,
+                    bias=1900.0 * OE, bias_direction=(0, 1, 0)),
+               dict(box=(6, 8, 0, 12, 0, 10), sigma=5e5),
+               dict(box=(9, 13, 4, 9, 3, 8), eps_r=13.0, Ms=1.3926e5, alpha=1e-2,
+                    bias=700.0 * OE, bias_direction=(1, 0, 1))],
+        source=dict(f0=70e9, Tp=0.6e-12, amplitude=3e8, location=(5, 6, 5),
+                    polarization=(0.0, 0.6, 0.8)),
+        boundaries=dict(x0="PMC", x1="MUR1", y0="PEC", y1="MUR1", z0="PMC",
+                        z1="MUR1"),
+        cfl=0.9, steps=120,
+        probes=[("Ez", 5, 6, 5), ("Mx", 3, 5, 4), ("My", 11, 6, 5), ("Hz", 10, 6, 5)],
+    ),
     # bias override through run(bias=...) along a tilted sweep direction
     "bias3d": dict(
         grid=(8, 9, 10, 6e-6, 6e-6, 6e-6),

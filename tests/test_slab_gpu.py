@@ -14,7 +14,8 @@ pytestmark = pytest.mark.gpu
 
 SPLITS = [("mixed3d", 2), ("mixed3d", 3), ("allmur3d", 2), ("allmur3d", 5),
           ("pec_block", 4), ("zwall_magnet", 2), ("zwall_magnet", 3), ("thin", 3),
-          ("plane2d", 2), ("xline1d", 4), ("bias3d", 2), ("plane_xz", 3)]
+          ("plane2d", 2), ("xline1d", 4), ("bias3d", 2), ("plane_xz", 3),
+          ("cpw_small", 3), ("two_magnets", 2), ("two_magnets", 4)]
 
 
 @pytest.mark.parametrize("name,nranks", SPLITS)
