@@ -207,6 +207,19 @@ CASES = {
         cfl=0.9, steps=120,
         probes=[("Ez", 5, 6, 5), ("Mx", 3, 5, 4), ("My", 11, 6, 5), ("Hz", 10, 6, 5)],
     ),
+    # StepFailure in 3D: many magnetic cells, a budget of 2 iterates and a
+    # tolerance no step can meet (the failure comes from the global rule)
+    "fail3d": dict(
+        grid=(9, 8, 7, 6e-6, 6e-6, 5e-6),
+        background=(0.0, 1.5),
+        boxes=[dict(box=(2, 7, 2, 6, 2, 5), eps_r=15.0, Ms=1.3926e5, alpha=1e-3,
+                    bias=1000.0 * OE, bias_direction=(0, 0, 1))],
+        source=dict(f0=60e9, Tp=0.5e-12, amplitude=1e8, location=(1, 4, 3),
+                    polarization=(0.0, 1.0, 0.0)),
+        boundaries=dict(x0="MUR1", x1="PEC", y0="PMC", y1="MUR1", z0="PEC", z1="MUR1"),
+        cfl=0.9, steps=100, llg=(1e-13, 2),
+        probes=[("Ey", 1, 4, 3), ("Mx", 4, 4, 3)],
+    ),
     # bias override through run(bias=...) along a tilted sweep direction
     "bias3d": dict(
         grid=(8, 9, 10, 6e-6, 6e-6, 6e-6),

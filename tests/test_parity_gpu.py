@@ -38,10 +38,11 @@ def test_gpu_matches_reference_golden(name, variant):
     _assert_same(res, load(name))
 
 
+@pytest.mark.parametrize("name", ["fail_tol", "fail3d"])
 @pytest.mark.parametrize("variant", VARIANTS)
-def test_gpu_step_failure(variant):
-    g = load("fail_tol")
-    cfg = build(CASES["fail_tol"], mirror_namespace())
+def test_gpu_step_failure(variant, name):
+    g = load(name)
+    cfg = build(CASES[name], mirror_namespace())
     with pytest.raises(llg.StepFailure) as ei:
         sim.run(cfg, kernel_variant=variant)
     assert ei.value.step == int(g["fail_step"])

@@ -78,3 +78,18 @@ def test_slab_group_benchmark_geometry(name, nranks, steps):
     assert np.array_equal(its, one.iterations[start:])
     for key in keys:
         assert np.array_equal(probes[key], one.probes[key].samples[start:]), key
+
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_slab_group_step_failure(nranks):
+    """The global stop rule fails across slabs exactly where the reference
+    raises StepFailure (same step, residual, iterate count)."""
+    g = load("fail3d")
+    cfg = build(CASES["fail3d"], mirror_namespace())
+    fields, M, probes, fail = parallel.run_group(cfg, nranks)
+    assert fields is None
+    step, residual, iterations, kind = fail
+    assert step == int(g["fail_step"])
+    assert residual == float(g["fail_residual"])
+    assert iterations == int(g["fail_iterations"])
