@@ -43,7 +43,9 @@ CASES = {
         boundaries=dict(x0="MUR1", x1="MUR1", y0="MUR1", y1="MUR1",
                         z0="MUR1", z1="MUR1"),
         cfl=0.95, steps=200,
-        probes=[("Ez", 1, 1, 2), ("My", 5, 4, 5), ("Hy", 0, 0, 0)],
+        probes=[("Ez", 1, 1, 2), ("My", 5, 4, 5), ("Hy", 0, 0, 0),
+                # M outside the magnet (a constant) and an H padding entry
+                ("Mz", 0, 0, 0), ("Hz", 10, 9, 0), ("Ex", 9, 9, 11)],
     ),
     # C1 in miniature: PEC box, YIG block, strong drive (mixed per-cell r_c)
     "pec_block": dict(
