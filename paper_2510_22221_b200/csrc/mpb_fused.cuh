@@ -106,17 +106,36 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
                         fs->smem);
     // x-chunks: ~32 (16) waves of two (one) CTAs per SM, chunks of >= 8 planes
     const int Fx = g.c1 - g.c0;                      // owned planes of this rank
-    int waves = fs->NT == 256 ? 32 : 16;
-    if (const char* e = getenv("MPB_SWEEP_WAVES")) waves = std::max(1, atoi(e));
-    const int want = std::max(1, (waves * sms + sc.tiles - 1) / sc.tiles);
-    // >= 8 planes per chunk (the pipeline fill is 3 planes), or >= 4 when
-    // 8-plane chunks would not even give two waves of CTAs (small grids,
-    // C1: +14%)
+    // x-chunks: the count that maximises (CTA slots kept busy over the whole
+    // grid of waves) x (useful planes / (planes + ~3 of halo plane and
+    // pipeline fill)) -- whole waves and long chunks (C4: 8 chunks = 7.0
+    // waves, +2% over a fixed 32-wave split; C2 +7%, C3 +3%, C5 +3%)
     const int per_sm = fs->NT == 256 ? 2 : 1;
-    int minch = sc.tiles * (Fx / 8) < 2 * per_sm * sms ? 4 : 8;
+    const double slots = (double)per_sm * sms;
+    int minch = 4;
     if (const char* e = getenv("MPB_SWEEP_MINCHUNK")) minch = std::max(2, atoi(e));
     const int maxch = std::max(1, Fx / minch);
-    sc.nchunks = std::max(1, std::min(want, maxch));
+    {
+        double best = -1.0;
+        for (int n = 1; n <= maxch; ++n) {
+            const int len = (Fx + n - 1) / n;
+            const int used = (Fx + len - 1) / len;              // chunks actually made
+            const double ctas = (double)sc.tiles * used;
+            // slabs with an overlapped exchange launch the interior chunks and
+            // the two edge chunks separately: count both launches' waves
+            const bool split = h->nranks > 1 && h->overlap && used > 2;
+            const double waves =
+                split ? std::ceil(sc.tiles * (used - 2.0) / slots) + std::ceil(sc.tiles * 2.0 / slots)
+                      : std::ceil(ctas / slots);
+            const double eff = ctas / (waves * slots) * ((double)len / (len + 3.0));
+            if (eff > best + 1e-9) { best = eff; sc.nchunks = used; }
+        }
+    }
+    if (const char* e = getenv("MPB_SWEEP_WAVES")) {        // the earlier fixed-wave rule
+        const int want = std::max(1, (std::max(1, atoi(e)) * sms + sc.tiles - 1) / sc.tiles);
+        sc.nchunks = std::max(1, std::min(want, maxch));
+    }
+    if (const char* e = getenv("MPB_SWEEP_CHUNKS")) sc.nchunks = std::max(1, atoi(e));
     sc.chunk = (Fx + sc.nchunks - 1) / sc.nchunks;
     sc.nchunks = (Fx + sc.chunk - 1) / sc.chunk;
     sc.ch_base = 0;
