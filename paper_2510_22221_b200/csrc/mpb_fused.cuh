@@ -104,7 +104,6 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
     if (fs->smem + static_smem > (size_t)smem_optin)
         return fail_msg(MPB_EINVAL, "fused sweep staging (%zu B) exceeds shared memory",
                         fs->smem);
-    // x-chunks: ~32 (16) waves of two (one) CTAs per SM, chunks of >= 8 planes
     const int Fx = g.c1 - g.c0;                      // owned planes of this rank
     // x-chunks: the count that maximises (CTA slots kept busy over the whole
     // grid of waves) x (useful planes / (planes + ~3 of halo plane and
