@@ -117,12 +117,12 @@ struct mpb_handle {
     LineProbe* lprobes = nullptr;
     cudaStream_t comm_stream = nullptr;
     cudaEvent_t ev_post = nullptr, ev_exch = nullptr;
-    // host copy of M on the local cell planes (cells outside the device M
-    // range never change)
     // M of the cell planes outside the device's magnetic planes [mx0, mx1)
     // (constant: only magnetic cells evolve); empty when it is all zero,
     // the normal case -- saves 3 doubles/cell of host memory on large grids
     std::vector<double> hostM;
+    // MPB_GUARD=1: allocation base and size of every guarded dev_alloc buffer
+    std::vector<std::pair<void*, size_t>> guarded;
     // timing
     int timing = 0;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events;
@@ -174,18 +174,70 @@ const uint8_t* ids_view(const mpb_handle* h) { return view(h->ids, h); }
 // Stream-ordered allocations on the handle's stream: neither allocating nor
 // freeing a handle synchronises the device, so concurrent runs on one GPU
 // (bias sweeps) do not stall each other's kernels.
+//
+// Debug mode MPB_GUARD=1 (the device-side bounds check; see tools/guard_tests.sh):
+// each buffer gets a kGuardBytes band of 0xA5 bytes on both sides.  dev_free
+// checks the bands and aborts the process if a kernel wrote outside its
+// buffer; a stray read of a band yields a garbage value that breaks the
+// bit-exact parity tests.
+constexpr size_t kGuardBytes = 4096;
+constexpr unsigned char kGuardByte = 0xA5;
+
+bool guard_mode() {
+    static const bool on = [] {
+        const char* e = getenv("MPB_GUARD");
+        const bool g = e && e[0] == '1';
+        if (g) fprintf(stderr, "MPB_GUARD: on (%zu-byte bands)\n", kGuardBytes);
+        return g;
+    }();
+    return on;
+}
+
 template <typename T>
 int dev_alloc(mpb_handle* h, T** p, size_t count) {
     if (count == 0) { *p = nullptr; return MPB_OK; }
-    CU(cudaMallocAsync(reinterpret_cast<void**>(p), count * sizeof(T), h->stream));
-    CU(cudaMemsetAsync(*p, 0, count * sizeof(T), h->stream));
+    const size_t bytes = count * sizeof(T);
+    if (guard_mode()) {
+        unsigned char* raw = nullptr;
+        CU(cudaMallocAsync(reinterpret_cast<void**>(&raw), bytes + 2 * kGuardBytes, h->stream));
+        CU(cudaMemsetAsync(raw, kGuardByte, bytes + 2 * kGuardBytes, h->stream));
+        CU(cudaMemsetAsync(raw + kGuardBytes, 0, bytes, h->stream));
+        *p = reinterpret_cast<T*>(raw + kGuardBytes);
+        h->guarded.emplace_back(raw, bytes);
+    } else {
+        CU(cudaMallocAsync(reinterpret_cast<void**>(p), bytes, h->stream));
+        CU(cudaMemsetAsync(*p, 0, bytes, h->stream));
+    }
     CU(cudaStreamSynchronize(h->stream));   // ready for synchronous copies
-    h->bytes += (int64_t)(count * sizeof(T));
+    h->bytes += (int64_t)bytes;
     return MPB_OK;
 }
 
 void dev_free(mpb_handle* h, void* p) {
-    if (p) cudaFreeAsync(p, h->stream);
+    if (!p) return;
+    if (guard_mode()) {
+        for (auto it = h->guarded.begin(); it != h->guarded.end(); ++it) {
+            unsigned char* raw = static_cast<unsigned char*>(it->first);
+            if (raw + kGuardBytes != p) continue;
+            std::vector<unsigned char> band(2 * kGuardBytes);
+            cudaStreamSynchronize(h->stream);
+            cudaMemcpy(band.data(), raw, kGuardBytes, cudaMemcpyDeviceToHost);
+            cudaMemcpy(band.data() + kGuardBytes, raw + kGuardBytes + it->second, kGuardBytes,
+                       cudaMemcpyDeviceToHost);
+            for (size_t b = 0; b < band.size(); ++b)
+                if (band[b] != kGuardByte) {
+                    fprintf(stderr, "MPB_GUARD: %s guard band of a %zu-byte buffer overwritten "
+                            "at byte %zd\n", b < kGuardBytes ? "low" : "high", it->second,
+                            b < kGuardBytes ? (ssize_t)b - (ssize_t)kGuardBytes
+                                            : (ssize_t)(it->second + b - kGuardBytes));
+                    abort();
+                }
+            cudaFreeAsync(raw, h->stream);
+            h->guarded.erase(it);
+            return;
+        }
+    }
+    cudaFreeAsync(p, h->stream);
 }
 
 int reset_state(mpb_handle* h) {
@@ -1084,10 +1136,10 @@ int mpb_run(mpb_handle* h, int64_t n0, int64_t nsteps, const double* src_vals,
     if (cap > h->stage_cap) {
         dev_free(h, h->d_src); dev_free(h, h->d_probe); dev_free(h, h->d_iters);
         h->d_src = nullptr; h->d_probe = nullptr; h->d_iters = nullptr;
-        CU(cudaMallocAsync(&h->d_src, cap * sizeof(double), h->stream));
-        CU(cudaMallocAsync(&h->d_probe, cap * std::max(1, h->nprobes) * sizeof(double),
-                           h->stream));
-        CU(cudaMallocAsync(&h->d_iters, cap * sizeof(int), h->stream));
+        int rc = dev_alloc(h, &h->d_src, (size_t)cap);
+        if (!rc) rc = dev_alloc(h, &h->d_probe, (size_t)(cap * std::max(1, h->nprobes)));
+        if (!rc) rc = dev_alloc(h, &h->d_iters, (size_t)cap);
+        if (rc) return rc;
         h->stage_cap = cap;
     }
     int64_t launches = 0;
