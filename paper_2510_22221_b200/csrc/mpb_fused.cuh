@@ -82,10 +82,62 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
     }
     if (const char* e = getenv("MPB_SWEEP_NT"))
         if (atoi(e) == 512) fs->NT = kSweepThreads;
-    sc.T = fs->V * fs->NT;
+    // x-chunks: for a tile count, the chunk count that maximises (CTA slots
+    // kept busy over the whole grid of waves) x (useful planes / (planes + ~3
+    // of halo plane and pipeline fill)) -- whole waves and long chunks (C4: 8
+    // chunks = 7.0 waves, +2% over a fixed 32-wave split; C2 +7%, C3 +3%, C5 +3%)
+    const int Fx = g.c1 - g.c0;                      // owned planes of this rank
+    const int per_sm = fs->NT == 256 ? 2 : 1;
+    const double slots = (double)per_sm * sms;
+    int minch = 4;
+    if (const char* e = getenv("MPB_SWEEP_MINCHUNK")) minch = std::max(2, atoi(e));
+    const int maxch = std::max(1, Fx / minch);
+    auto chunks_for = [&](int tiles, double* waves_out) {
+        double best = -1.0;
+        int pick = 1;
+        for (int n = 1; n <= maxch; ++n) {
+            const int len = (Fx + n - 1) / n;
+            const int used = (Fx + len - 1) / len;              // chunks actually made
+            const double ctas = (double)tiles * used;
+            // slabs with an overlapped exchange launch the interior chunks and
+            // the two edge chunks separately: count both launches' waves
+            const bool split = h->nranks > 1 && h->overlap && used > 2;
+            const double waves =
+                split ? std::ceil(tiles * (used - 2.0) / slots) + std::ceil(tiles * 2.0 / slots)
+                      : std::ceil(ctas / slots);
+            const double eff = ctas / (waves * slots) * ((double)len / (len + 3.0));
+            if (eff > best + 1e-9) { best = eff; pick = used; *waves_out = waves; }
+        }
+        return pick;
+    };
+    // tile size: the full V x NT tile, unless a smaller even tile lets the
+    // tiles x chunks grid fill its last wave with >2% less modelled time.
+    // Model: waves x (chunk planes + 3) x (per-plane latency + T), the latency
+    // worth ~1400 entries of streaming (fitted to A/B runs: a CTA's time per
+    // plane is mostly the wait for its staged plane, little of it scales with
+    // T).  Planes of ~17K entries (C2, C3) leave a tenth of the wave idle with
+    // 512-entry tiles; 452/458-entry tiles fill it (+3% measured).  C4 and C5
+    // keep the full tile.
+    const int Tmax = fs->V * fs->NT;
+    auto model = [&](int T, int* nch) {
+        double waves = 1.0;
+        *nch = chunks_for((g.FyFz + T - 1) / T, &waves);
+        return waves * (1400.0 + T) * (((Fx + *nch - 1) / *nch) + 3.0);
+    };
+    sc.T = Tmax;
     if (const char* e = getenv("MPB_SWEEP_T")) {   // even: 16-byte aligned tile starts
         const int t = atoi(e) & ~1;
         if (t > 0 && t <= sc.T) sc.T = t;
+    } else {
+        int nch = 1;
+        const double full = model(Tmax, &nch);
+        double best = full;
+        int bestT = Tmax;
+        for (int T = Tmax - 2; T >= Tmax / 2; T -= 2) {
+            const double t = model(T, &nch);
+            if (t < best - 1e-9) { best = t; bestT = T; }
+        }
+        if (best < full / 1.02) sc.T = bestT;
     }
     sc.tiles = (g.FyFz + sc.T - 1) / sc.T;
     {
@@ -104,31 +156,9 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
     if (fs->smem + static_smem > (size_t)smem_optin)
         return fail_msg(MPB_EINVAL, "fused sweep staging (%zu B) exceeds shared memory",
                         fs->smem);
-    const int Fx = g.c1 - g.c0;                      // owned planes of this rank
-    // x-chunks: the count that maximises (CTA slots kept busy over the whole
-    // grid of waves) x (useful planes / (planes + ~3 of halo plane and
-    // pipeline fill)) -- whole waves and long chunks (C4: 8 chunks = 7.0
-    // waves, +2% over a fixed 32-wave split; C2 +7%, C3 +3%, C5 +3%)
-    const int per_sm = fs->NT == 256 ? 2 : 1;
-    const double slots = (double)per_sm * sms;
-    int minch = 4;
-    if (const char* e = getenv("MPB_SWEEP_MINCHUNK")) minch = std::max(2, atoi(e));
-    const int maxch = std::max(1, Fx / minch);
     {
-        double best = -1.0;
-        for (int n = 1; n <= maxch; ++n) {
-            const int len = (Fx + n - 1) / n;
-            const int used = (Fx + len - 1) / len;              // chunks actually made
-            const double ctas = (double)sc.tiles * used;
-            // slabs with an overlapped exchange launch the interior chunks and
-            // the two edge chunks separately: count both launches' waves
-            const bool split = h->nranks > 1 && h->overlap && used > 2;
-            const double waves =
-                split ? std::ceil(sc.tiles * (used - 2.0) / slots) + std::ceil(sc.tiles * 2.0 / slots)
-                      : std::ceil(ctas / slots);
-            const double eff = ctas / (waves * slots) * ((double)len / (len + 3.0));
-            if (eff > best + 1e-9) { best = eff; sc.nchunks = used; }
-        }
+        double waves = 1.0;
+        sc.nchunks = chunks_for(sc.tiles, &waves);
     }
     if (const char* e = getenv("MPB_SWEEP_WAVES")) {        // the earlier fixed-wave rule
         const int want = std::max(1, (std::max(1, atoi(e)) * sms + sc.tiles - 1) / sc.tiles);
