@@ -113,6 +113,9 @@ struct mpb_handle {
     bool exch_pending = false;
     // lines along z: the whole run in one shared-memory-resident CTA (mpb_line.cuh)
     bool line = false;
+    // MPB_WALLS=face: x/y walls as one k_wall launch per face (the unfused
+    // form, kept for the parity tests of k_walls_xy)
+    bool wall_per_face = false;
     size_t line_smem = 0;
     LineProbe* lprobes = nullptr;
     cudaStream_t comm_stream = nullptr;
@@ -382,8 +385,25 @@ int phase_post(mpb_handle* h, int pa, cudaStream_t s, int64_t& launches,
         k_esweep<<<plane_grid, 256, 0, s>>>(g, b, h->mats, ids, h->st);
         ++launches;
     }
+    // x and y walls: one launch for the four faces (k_walls_xy); z walls
+    // are in the sweep (+ k_zfix) or, unfused, one k_wall launch per face
+    {
+        int act = 0;
+        int64_t cnt = 0;
+        for (int face = 0; face < 4; ++face)
+            if (h->faces_active[face]) {
+                act |= 1 << face;
+                cnt = std::max<int64_t>(cnt, face < 2 ? (int64_t)g.F[1] * g.F[2]
+                                                      : (int64_t)(g.c1 - g.c0) * g.F[2]);
+            }
+        if (act && !h->wall_per_face) {
+            k_walls_xy<<<dim3((unsigned)((cnt + 255) / 256), 4), 256, 0, s>>>(g, b, h->mats, ids,
+                                                                              h->st, act);
+            ++launches;
+        }
+    }
     const int nface = g.zin ? 4 : 6;   // fused: z walls are in the sweep
-    for (int face = 0; face < nface; ++face) {
+    for (int face = h->wall_per_face ? 0 : 4; face < nface; ++face) {
         if (!h->faces_active[face]) continue;
         const int axis = face >> 1;
         const int u = axis == 0 ? 1 : 0, w = axis == 2 ? 1 : 2;
@@ -788,6 +808,8 @@ int mpb_create(const mpb_setup* su, mpb_handle** out) {
     g.max_iters = su->llg_max_iters;
     g.tol = su->llg_tol;
     g.zin = su->kernel_variant == 1 ? 0 : 1;
+    if (const char* e = getenv("MPB_WALLS"))        // "face": one x/y wall launch per face
+        h->wall_per_face = !strcmp(e, "face");
     if (const char* e = getenv("MPB_ZWALL"))        // "kernel": separate z-wall launches
         if (!strcmp(e, "kernel")) g.zin = 0;
     g.c0 = x_lo;

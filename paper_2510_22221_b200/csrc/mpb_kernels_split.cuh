@@ -427,6 +427,69 @@ __global__ void __launch_bounds__(256) k_wall(Geom g, Bufs b,
     }
 }
 
+// The x0, x1, y0, y1 walls in ONE launch (blockIdx.y = face), with the
+// result of the sequential face order (em.py:324-359).  The faces interact
+// only on the edge lines: y walls overwrite Ez on the x walls' j = 0 / ny
+// rows (so the x-face thread skips those entries), and a y wall's MUR reads
+// Ez at its inner row, which an x wall has already written on i = 0 / nx (so
+// the y-face thread recomputes the x wall's value there instead of reading
+// it).  Every other read is of entries no wall writes.  act: bit f = face f
+// active on this rank.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double wall_value(const Geom& g, const Bufs& b,
+                                             const mpb_material* __restrict__ mats,
+                                             const uint8_t* __restrict__ ids, int face, int c,
+                                             int64_t ow, int64_t oi) {
+    if (g.faces[face] == MPB_FACE_PEC) return 0.0;
+    // MUR1: wall = prev_inner + k (inner_new - prev_wall)
+    const double kk = mats[ids[ow]].mur_k[face >> 1];
+    return b.Ea[c][oi] + kk * (b.Eb[c][oi] - b.Ea[c][ow]);
+}
+
+__global__ void __launch_bounds__(256) k_walls_xy(Geom g, Bufs b,
+                                                  const mpb_material* __restrict__ mats,
+                                                  const uint8_t* __restrict__ ids,
+                                                  const StepState* st, int act) {
+    const int face = blockIdx.y;
+    if (st->fail || !((act >> face) & 1)) return;
+    const int side = face & 1;
+    const int Fz = g.F[2];
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (face < 2) {                            // x wall: entries (j, k), Ey and Ez
+        if (t >= (int64_t)g.F[1] * Fz) return;
+        const int j = (int)(t / Fz);
+        const int64_t ow = (int64_t)(side ? g.n[0] : 0) * g.PP + t;
+        const int64_t oi = (int64_t)(side ? g.n[0] - 1 : 1) * g.PP + t;
+        b.Eb[1][ow] = wall_value(g, b, mats, ids, face, 1, ow, oi);
+        const bool y_over = (j == 0 && (act & 4)) || (j == g.n[1] && (act & 8));
+        if (!y_over) b.Eb[2][ow] = wall_value(g, b, mats, ids, face, 2, ow, oi);
+    } else {                                   // y wall: entries (i, k) of owned planes, Ex and Ez
+        const int nown = g.c1 - g.c0;
+        if (t >= (int64_t)nown * Fz) return;
+        const int i = g.c0 + (int)(t / Fz);
+        const int k = (int)(t - (int64_t)(i - g.c0) * Fz);
+        const int jw = side ? g.n[1] : 0, jn = side ? g.n[1] - 1 : 1;
+        const int64_t ow = (int64_t)i * g.PP + (int64_t)jw * Fz + k;
+        const int64_t oi = (int64_t)i * g.PP + (int64_t)jn * Fz + k;
+        b.Eb[0][ow] = wall_value(g, b, mats, ids, face, 0, ow, oi);
+        // Ez at the inner row, after the x walls
+        double ez_in;
+        const int xf = (i == 0 && (act & 1)) ? 0 : ((i == g.n[0] && (act & 2)) ? 1 : -1);
+        if (xf >= 0) {
+            const int64_t xin = (int64_t)(xf ? g.n[0] - 1 : 1) * g.PP + (int64_t)jn * Fz + k;
+            ez_in = wall_value(g, b, mats, ids, xf, 2, oi, xin);
+        } else {
+            ez_in = b.Eb[2][oi];
+        }
+        if (g.faces[face] == MPB_FACE_PEC) {
+            b.Eb[2][ow] = 0.0;
+        } else {
+            const double kk = mats[ids[ow]].mur_k[1];
+            b.Eb[2][ow] = b.Ea[2][oi] + kk * (ez_in - b.Ea[2][ow]);
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Energy diagnostic (em.py:366-383): per-block partial sums in a fixed
 // order, then one block combines them -- deterministic run to run.
