@@ -120,24 +120,34 @@ __device__ __forceinline__ E3 e_plain_at(const Geom& g, const Bufs& b,
     const bool p[6] = {g.faces[0] == MPB_FACE_PMC, g.faces[1] == MPB_FACE_PMC,
                        g.faces[2] == MPB_FACE_PMC, g.faces[3] == MPB_FACE_PMC,
                        g.faces[4] == MPB_FACE_PMC, g.faces[5] == MPB_FACE_PMC};
-    if (g.act[1]) {   // cHx += dHz/dy ; cHz -= dHx/dy
-        cx = cx + bwd_diff(H[2], o, sy, j, g.n[1], g.d[1], g.rd[1], p[2], p[3]);
-        cz = cz - bwd_diff(H[0], o, sy, j, g.n[1], g.d[1], g.rd[1], p[2], p[3]);
-    }
-    if (g.act[2]) {   // cHx -= dHy/dz ; cHy += dHx/dz
-        cx = cx - bwd_diff(H[1], o, 1, k, g.n[2], g.d[2], g.rd[2], p[4], p[5]);
-        cy = cy + bwd_diff(H[0], o, 1, k, g.n[2], g.d[2], g.rd[2], p[4], p[5]);
-    }
-    if (g.act[0]) {   // cHy -= dHz/dx ; cHz += dHy/dx
-        cy = cy - bwd_diff(H[2], o, sx, i, g.n[0], g.d[0], g.rd[0], p[0], p[1]);
-        cz = cz + bwd_diff(H[1], o, sx, i, g.n[0], g.d[0], g.rd[0], p[0], p[1]);
-    }
+    // every load first (see curl_e_at); same differences in the same order
+    const bool ay = g.act[1], az = g.act[2], ax = g.act[0];
+    const double h0 = H[0][o], h1 = H[1][o], h2 = H[2][o];
+    const double h2_y = ay ? bwd_lo_load(H[2], o, sy, j) : 0.0;
+    const double h0_y = ay ? bwd_lo_load(H[0], o, sy, j) : 0.0;
+    const double h1_z = az ? bwd_lo_load(H[1], o, 1, k) : 0.0;
+    const double h0_z = az ? bwd_lo_load(H[0], o, 1, k) : 0.0;
+    const double h2_x = ax ? bwd_lo_load(H[2], o, sx, i) : 0.0;
+    const double h1_x = ax ? bwd_lo_load(H[1], o, sx, i) : 0.0;
+    const double e0 = b.Ea[0][o], e1 = b.Ea[1][o], e2 = b.Ea[2][o];
     const uint8_t id = ids[o];
     const double ca = mats[id].ca, cb = mats[id].cb;
+    if (ay) {   // cHx += dHz/dy ; cHz -= dHx/dy
+        cx = cx + bwd_diff_v(h2, h2_y, j, g.n[1], g.d[1], g.rd[1], p[2], p[3]);
+        cz = cz - bwd_diff_v(h0, h0_y, j, g.n[1], g.d[1], g.rd[1], p[2], p[3]);
+    }
+    if (az) {   // cHx -= dHy/dz ; cHy += dHx/dz
+        cx = cx - bwd_diff_v(h1, h1_z, k, g.n[2], g.d[2], g.rd[2], p[4], p[5]);
+        cy = cy + bwd_diff_v(h0, h0_z, k, g.n[2], g.d[2], g.rd[2], p[4], p[5]);
+    }
+    if (ax) {   // cHy -= dHz/dx ; cHz += dHy/dx
+        cy = cy - bwd_diff_v(h2, h2_x, i, g.n[0], g.d[0], g.rd[0], p[0], p[1]);
+        cz = cz + bwd_diff_v(h1, h1_x, i, g.n[0], g.d[0], g.rd[0], p[0], p[1]);
+    }
     E3 r;
-    r.x = ca * (cx - cb * b.Ea[0][o]);
-    r.y = ca * (cy - cb * b.Ea[1][o]);
-    r.z = ca * (cz - cb * b.Ea[2][o]);
+    r.x = ca * (cx - cb * e0);
+    r.y = ca * (cy - cb * e1);
+    r.z = ca * (cz - cb * e2);
     return r;
 }
 

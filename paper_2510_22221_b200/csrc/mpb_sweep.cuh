@@ -484,7 +484,10 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
 // curl E, H^n, M^n) and writes H^{n+1}, M^{n+1}; per-block residual history and
 // local-stop range feed the global stop rule (k_llg_fixup / all-reduce).
 // Ghost-plane copies (slabs) are computed for their H only.
-__global__ void __launch_bounds__(256, 3) k_llg_local(Geom g, Bufs b,
+#ifndef MPB_LLG_MINB
+#define MPB_LLG_MINB 3
+#endif
+__global__ void __launch_bounds__(256, MPB_LLG_MINB) k_llg_local(Geom g, Bufs b,
                                                    const mpb_material* __restrict__ mats,
                                                    const uint8_t* __restrict__ ids,
                                                    const int2* __restrict__ cells,
@@ -502,10 +505,13 @@ __global__ void __launch_bounds__(256, 3) k_llg_local(Geom g, Bufs b,
         const int64_t o = i * g.PP + f;
         const int64_t om = (int64_t)(i - g.mx0) * g.PP + f;
         LlgCell s;
-        const Curl3 c = curl_e_at(g, b.Ea, o, g.PP, g.F[2], true, true, true);
+        // H^n, M^n and the material id are loaded before the curl's divisions
+        // (see curl_e_at) so every load of the cell is in flight at once
         for (int k = 0; k < 3; ++k) { s.Hn[k] = b.Ha[k][o]; s.Mn[k] = b.Ma[k][om]; }
+        const uint8_t id = ids[o];
+        const Curl3 c = curl_e_at(g, b.Ea, o, g.PP, g.F[2], true, true, true);
         s.cE[0] = c.x; s.cE[1] = c.y; s.cE[2] = c.z;
-        llg_setup(s, mats[ids[o]]);
+        llg_setup(s, mats[id]);
         const bool own = owned[q] != 0;
         double Hr[3] = {s.Hn[0], s.Hn[1], s.Hn[2]};
         double Mr[3] = {s.Mn[0], s.Mn[1], s.Mn[2]};
