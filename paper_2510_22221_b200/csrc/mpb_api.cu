@@ -107,6 +107,7 @@ struct mpb_handle {
     int64_t stage_cap = 0;
     cudaStream_t stream = nullptr;
     cudaGraphExec_t graph[2] = {nullptr, nullptr};
+    int64_t graph_launches[2] = {0, 0};   // kernels captured in each graph
     // slab exchange overlapped with the next step's interior sweep: the
     // exchange runs on comm_stream after ev_post, the edge chunks wait ev_exch
     bool overlap = false;
@@ -562,6 +563,7 @@ int build_graph(mpb_handle* h, int start_parity) {
     const int64_t saved = h->launches_last;
     for (int s = 0; s < h->graph_steps && rc == MPB_OK; ++s)
         rc = enqueue_step(h, (start_parity + s) & 1, false);
+    h->graph_launches[start_parity] = h->launches_last - saved;
     h->launches_last = saved;
     cudaError_t e = cudaStreamEndCapture(h->stream, &graph);
     if (rc) return rc;
@@ -570,16 +572,6 @@ int build_graph(mpb_handle* h, int start_parity) {
     CU(cudaGraphInstantiate(&h->graph[start_parity], graph, 0));
     CU(cudaGraphDestroy(graph));
     return MPB_OK;
-}
-
-int64_t launches_per_step(mpb_handle* h) {
-    int64_t n = (h->variant == 1 ? 2 : 1) + 1;
-    if (h->nranks == 1 && h->nmag > 0) n += 1;
-    if (h->nranks > 1 && h->any_magnetic) n += 1 + (h->nmag > 0 ? 1 : 0);
-    if (h->variant != 1 && h->nmag > 0) n += 2;   // k_llg_local + k_edefer
-    for (int f = 0; f < (h->g.zin ? 4 : 6); ++f) n += h->faces_active[f];
-    if (h->g.zin) n += zfix_launches(h);
-    return n;
 }
 
 // Enqueue nsteps steps; buffers already pointed to by the device state.
@@ -596,7 +588,7 @@ int enqueue_steps(mpb_handle* h, int64_t nsteps) {
                 if (rc) return rc;
             }
             CU(cudaGraphLaunch(h->graph[h->parity], h->stream));
-            h->launches_last += launches_per_step(h) * h->graph_steps;
+            h->launches_last += h->graph_launches[h->parity];
             if (h->graph_steps & 1) h->parity ^= 1;
             s += h->graph_steps;
         } else {

@@ -50,3 +50,25 @@ def test_benchmark_size_runs_are_deterministic(name, steps):
     a = _digest_run(cfg, state, 100, steps)
     b = _digest_run(cfg, state, 100, steps)
     assert a == b
+
+
+@pytest.mark.parametrize("name", ["c1", "c3"])
+def test_graph_and_eager_launch_counts_agree(name):
+    """The launch count reported for CUDA-graph replays (bench `gpu_launches`,
+    e2e leg) is the number of kernels captured, i.e. the eager count."""
+    cfg = load_config(ROOT / "configs" / f"{name}.cfg")
+    keys = list(dict.fromkeys((p[0], (p[1], p[2], p[3])) for p in cfg.probes))
+    counts = []
+    for timed in (True, False):          # timed: eager launches; else graphs
+        dev = sim._device_run(cfg, cfg.materials, keys)
+        try:
+            fs = cfg.grid.field_shape
+            dev.load_state({k: np.zeros(fs) for k in ("Ex", "Ey", "Ez", "Hx", "Hy", "Hz")},
+                           initial_magnetization(cfg.materials))
+            dev.set_kernel_timing(timed)
+            _, _, fail = dev.run(0, sim.source_values(cfg.source, cfg.dt, 0, 32))
+            assert fail is None
+            counts.append(dev.launch_count())
+        finally:
+            dev.close()
+    assert counts[0] == counts[1] > 0, counts
