@@ -117,6 +117,7 @@ struct mpb_handle {
     // MPB_WALLS=face: x/y walls as one k_wall launch per face (the unfused
     // form, kept for the parity tests of k_walls_xy)
     bool wall_per_face = false;
+    bool pdl = true;          // programmatic dependent launch of the step's tail (MPB_PDL=0: off)
     size_t line_smem = 0;
     LineProbe* lprobes = nullptr;
     cudaStream_t comm_stream = nullptr;
@@ -398,8 +399,9 @@ int phase_post(mpb_handle* h, int pa, cudaStream_t s, int64_t& launches,
                                                       : (int64_t)(g.c1 - g.c0) * g.F[2]);
             }
         if (act && !h->wall_per_face) {
-            k_walls_xy<<<dim3((unsigned)((cnt + 255) / 256), 4), 256, 0, s>>>(g, b, h->mats, ids,
-                                                                              h->st, act);
+            CU(launch_pdl(h->pdl, k_walls_xy, dim3((unsigned)((cnt + 255) / 256), 4), dim3(256),
+                          s, g, b, (const mpb_material*)h->mats, ids, (const StepState*)h->st,
+                          act));
             ++launches;
         }
     }
@@ -418,8 +420,9 @@ int phase_post(mpb_handle* h, int pa, cudaStream_t s, int64_t& launches,
         if (rc) return rc;
         launches += zfix_launches(h);
     }
-    k_finish<<<1, 256, 0, s>>>(g, b, h->src, h->probes, h->nprobes, 1 - pa,
-                               h->any_magnetic ? 1 : 0, h->st);
+    CU(launch_pdl(h->pdl, k_finish, dim3(1), dim3(256), s, g, b, h->src,
+                  (const ProbeDesc*)h->probes, h->nprobes, 1 - pa,
+                  h->any_magnetic ? 1 : 0, h->st));
     ++launches;
     return MPB_OK;
 }
@@ -802,6 +805,7 @@ int mpb_create(const mpb_setup* su, mpb_handle** out) {
     g.zin = su->kernel_variant == 1 ? 0 : 1;
     if (const char* e = getenv("MPB_WALLS"))        // "face": one x/y wall launch per face
         h->wall_per_face = !strcmp(e, "face");
+    if (const char* e = getenv("MPB_PDL")) h->pdl = strcmp(e, "0") != 0;
     if (const char* e = getenv("MPB_ZWALL"))        // "kernel": separate z-wall launches
         if (!strcmp(e, "kernel")) g.zin = 0;
     g.c0 = x_lo;

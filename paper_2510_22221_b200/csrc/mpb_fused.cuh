@@ -240,8 +240,9 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
 int launch_zfix(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s) {
     FusedState* fs = fused_of(h);
     if (!fs->nzlines) return MPB_OK;
-    k_zfix<<<(fs->nzlines + 255) / 256, 256, 0, s>>>(g, b, h->mats, ids_view(h), fs->zlines,
-                                                     fs->nzlines, h->st);
+    CU(launch_pdl(h->pdl, k_zfix, dim3((fs->nzlines + 255) / 256), dim3(256), s, g, b,
+                  (const mpb_material*)h->mats, ids_view(h), (const int3*)fs->zlines,
+                  fs->nzlines, (const StepState*)h->st));
     return MPB_OK;
 }
 
@@ -303,8 +304,9 @@ int launch_fused(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s, in
 int launch_deferred(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s) {
     FusedState* fs = fused_of(h);
     if (!fs->ndefer) return MPB_OK;
-    k_edefer<<<(fs->ndefer + 255) / 256, 256, 0, s>>>(g, b, h->mats, ids_view(h), fs->defer,
-                                                    fs->ndefer, h->st, 1);
+    CU(launch_pdl(h->pdl, k_edefer, dim3((fs->ndefer + 255) / 256), dim3(256), s, g, b,
+                  (const mpb_material*)h->mats, ids_view(h), (const int2*)fs->defer,
+                  fs->ndefer, (const StepState*)h->st, 1));
     return MPB_OK;
 }
 

@@ -460,6 +460,8 @@ __global__ void __launch_bounds__(256) k_walls_xy(Geom g, Bufs b,
                                                   const mpb_material* __restrict__ mats,
                                                   const uint8_t* __restrict__ ids,
                                                   const StepState* st, int act) {
+    pdl_wait();
+    pdl_trigger();
     const int face = blockIdx.y;
     if (st->fail || !((act >> face) & 1)) return;
     const int side = face & 1;
@@ -554,6 +556,8 @@ __global__ void __launch_bounds__(256) k_finish(Geom g, Bufs b, SourceDesc src,
                                                 const ProbeDesc* __restrict__ probes,
                                                 int nprobes, int parity_b, int record_iters,
                                                 StepState* st) {
+    pdl_wait();
+    pdl_trigger();
     if (st->fail) return;
     const long long row = st->local;
     if (threadIdx.x == 0) {

@@ -540,6 +540,8 @@ __global__ void __launch_bounds__(256) k_edefer(Geom g, Bufs b,
                                                 const uint8_t* __restrict__ ids,
                                                 const int2* __restrict__ list, int n,
                                                 const StepState* st, int always) {
+    pdl_wait();
+    pdl_trigger();
     if (st->fail || (!always && !st->fixup_ran)) return;
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= n) return;
@@ -582,6 +584,8 @@ __global__ void __launch_bounds__(256) k_zfix(Geom g, Bufs b,
                                               const uint8_t* __restrict__ ids,
                                               const int3* __restrict__ lines, int n,
                                               const StepState* st) {
+    pdl_wait();
+    pdl_trigger();
     if (st->fail) return;
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= n) return;
