@@ -252,9 +252,10 @@ int zfix_launches(mpb_handle* h) { return fused_of(h)->nzlines ? 1 : 0; }
 int launch_llg_local(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s) {
     if (!h->nmag) return MPB_OK;
     const size_t smem = (size_t)(g.max_iters + 2) * sizeof(unsigned long long);
-    k_llg_local<<<(h->nmag + 255) / 256, 256, smem, s>>>(g, b, h->mats, ids_view(h),
-                                                        h->magcells, h->magowned, h->nmag,
-                                                        h->st);
+    CU(launch_pdl_smem(h->pdl, k_llg_local, dim3((h->nmag + 255) / 256), dim3(256), smem, s,
+                       g, b, (const mpb_material*)h->mats, ids_view(h),
+                       (const int2*)h->magcells, (const unsigned char*)h->magowned, h->nmag,
+                       h->st));
     return MPB_OK;
 }
 
@@ -285,11 +286,11 @@ int launch_fused(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s, in
     }
     ++launches;
 #define MPB_LAUNCH(VV, FF)                                                              \
-    k_sweep<VV, FF><<<grid, kSweepThreads, fs->smem, s>>>(g, b, h->mats, ids_view(h),     \
-                                                          h->st, sc)
+    CU(launch_pdl_smem(h->pdl, k_sweep<VV, FF>, dim3(grid), dim3(kSweepThreads), fs->smem, s,  \
+                       g, b, (const mpb_material*)h->mats, ids_view(h), h->st, sc))
     if (fs->NT == 256) {
-        k_sweep<2, true, 256><<<grid, 256, fs->smem, s>>>(g, b, h->mats, ids_view(h), h->st,
-                                                         sc);
+        CU(launch_pdl_smem(h->pdl, k_sweep<2, true, 256>, dim3(grid), dim3(256), fs->smem, s, g,
+                           b, (const mpb_material*)h->mats, ids_view(h), h->st, sc));
     } else if (fs->F3) {
         if (fs->V == 2) MPB_LAUNCH(2, true);
         else MPB_LAUNCH(1, true);

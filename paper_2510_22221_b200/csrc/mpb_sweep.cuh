@@ -226,6 +226,7 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
     __shared__ double s_murz[MPB_MAX_MATERIALS];
     unsigned char* ring = smem;
 
+    pdl_wait();   // launched behind the previous step's k_finish (see pdl_wait)
     if (st->fail) return;
     const int tid = threadIdx.x;
     const int tile = blockIdx.x % sc.tiles;
@@ -495,6 +496,8 @@ __global__ void __launch_bounds__(256, MPB_LLG_MINB) k_llg_local(Geom g, Bufs b,
                                                    int ncells, StepState* st) {
     extern __shared__ unsigned long long lhist[];
     __shared__ int lrc[2];
+    pdl_wait();
+    pdl_trigger();
     if (st->fail) return;
     CtaLlgStats cs{lhist, lrc};
     cta_stats_init(cs, g.max_iters);
