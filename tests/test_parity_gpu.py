@@ -115,6 +115,16 @@ def test_gpu_zwall_kernel_order_matches_golden(name, monkeypatch):
     _assert_same(res, load(name))
 
 
+# Plain stream-ordered launches instead of programmatic dependent launch
+# (MPB_PDL=0): the same kernels with full serialisation, same bits.
+@pytest.mark.parametrize("name", ["mixed3d", "allmur3d", "two_magnets"])
+def test_gpu_without_pdl_matches_golden(name, monkeypatch):
+    monkeypatch.setenv("MPB_PDL", "0")
+    case = CASES[name]
+    res = sim.run(build(case, mirror_namespace()), bias=case.get("bias"))
+    _assert_same(res, load(name))
+
+
 # Lines along z run in the shared-memory line kernel by default (k_line);
 # the general kernels must still give the same bits for them (MPB_LINE=0),
 # including the StepFailure case.
