@@ -343,11 +343,13 @@ int phase_fixup_single(mpb_handle* h, int pa, cudaStream_t s, int64_t& launches)
     cfg.gridDim = dim3(h->fixup_blocks);
     cfg.blockDim = dim3(256);
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = h->pdl ? 2 : 1;
     MagScratch scr{h->scratch};
     CU(cudaLaunchKernelEx(&cfg, k_llg_fixup, g, b, (const mpb_material*)h->mats, ids_view(h),
                           (const int2*)h->magcells, h->nmag, scr, h->st));

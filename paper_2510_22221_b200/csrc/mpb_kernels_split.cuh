@@ -195,6 +195,8 @@ __global__ void __launch_bounds__(256) k_llg_fixup(Geom g, Bufs b,
                                                    const int2* __restrict__ cells, int nmag,
                                                    MagScratch scr, StepState* st) {
     __shared__ unsigned long long red[32];
+    pdl_wait();
+    pdl_trigger();
     if (st->fail) return;
     const int rmin = -st->rc_negmin, rmax = st->rc_max;
     if (rmin == rmax && rmax <= g.max_iters) {
