@@ -151,7 +151,19 @@ def synthetic_state(fs, kind: str):
     return out
 
 
-def slab_run(cfg, keys, world, rank, local, args):
+def _device_class():
+    """engine.DeviceRun, or (tests only) the class named by MPB_BENCH_DEVICE
+    as "module:Class" -- lets a CPU test drive the multi-rank set-up."""
+    spec = os.environ.get("MPB_BENCH_DEVICE")
+    if spec:
+        import importlib
+        mod, cls = spec.split(":")
+        return getattr(importlib.import_module(mod), cls)
+    from paper_2510_22221_b200.engine import DeviceRun
+    return DeviceRun
+
+
+def slab_run(cfg, keys, world, rank, local, args, nccl: bool = True):
     """One rank's x-slab, NCCL exchange with its neighbours.
 
     weak (C4, BASELINE configs[3]): the global grid is the config's geometry
@@ -164,12 +176,11 @@ def slab_run(cfg, keys, world, rank, local, args):
     from dataclasses import replace
 
     from paper_2510_22221_b200 import parallel
-    from paper_2510_22221_b200.engine import DeviceRun
     from paper_2510_22221_b200.grid import GridSpec, initial_magnetization
     from paper_2510_22221_b200.sim import _device_run_args
 
     g = cfg.grid
-    nccl_id = parallel.nccl_unique_id(dist) if world > 1 else bytes(128)
+    nccl_id = parallel.nccl_unique_id(dist) if world > 1 and nccl else bytes(128)
     if args.scaling == "weak":
         ggrid = GridSpec(g.nx * world, g.ny, g.nz, g.dx, g.dy, g.dz)
         gcfg = replace(cfg, grid=ggrid, probes=())
@@ -182,7 +193,7 @@ def slab_run(cfg, keys, world, rank, local, args):
     mats = (cfg.materials.tiled_region(c0, c1) if args.scaling == "weak"
             else cfg.materials.region(c0, c1))
     a = _device_run_args(gcfg, keys)
-    dev = DeviceRun(ggrid, mats, a["boundaries"], a["source_loc"], a["source_pol"], keys,
+    dev = _device_class()(ggrid, mats, a["boundaries"], a["source_loc"], a["source_pol"], keys,
                     cfg.llg_params, cfg.dt, device=local, kernel_variant=args.variant,
                     slab=slab)
     f0, f1 = slab.field_range
@@ -192,114 +203,197 @@ def slab_run(cfg, keys, world, rank, local, args):
     return dev, (slab.x_hi - slab.x_lo) * g.ny * g.nz
 
 
-def cpu_oracle_sample(cfg_name: str, steps: int):
-    """Time the numpy oracle (restatement of the reference CPU path) on a
-    bounded sample; returns (Gcell-updates/s, description)."""
+def slab_sample_config(cfg, x0: int, x1: int):
+    """The config's cell planes [x0, x1) as a stand-alone config for the CPU
+    reference: same y-z geometry, materials and walls, the source only if it
+    lies in the slab (else a zero-amplitude one), no probes.  Per-cell work is that of the whole grid."""
     from dataclasses import replace
 
+    from paper_2510_22221_b200 import em
+    from paper_2510_22221_b200.grid import GridSpec
+    g = cfg.grid
+    sub = GridSpec(x1 - x0, g.ny, g.nz, g.dx, g.dy, g.dz)
+    mats = cfg.materials.region(x0, x1)
+    src = cfg.source
+    loc = src.location
+    if x0 <= loc[0] < x1:
+        src = replace(src, location=(loc[0] - x0, loc[1], loc[2]))
+    else:                        # same per-step work, nothing injected
+        src = replace(src, location=(0, loc[1], loc[2]), amplitude=0.0)
+    return replace(cfg, grid=sub, materials=mats, source=src, probes=())
+
+
+def _oracle_steps(cfg, warm: int, steps: int):
+    """Run the numpy oracle for warm + steps steps; returns the seconds of the
+    last `steps` (set-up and warm-up excluded)."""
     from oracle import magphon_oracle as orc
+    marks = []
+    orc.run(cfg, n_steps=warm + steps, marks=marks)
+    return marks[-1] - marks[warm]
+
+
+def cpu_oracle_sample(cfg_name: str, planes: int, steps: int):
+    """Time the numpy oracle (restatement of the reference CPU path) on one
+    host core over the first `planes` x-planes of the bench config; returns
+    (Gcell-updates/s, seconds, cells)."""
     from paper_2510_22221_b200.config import load_config
-    cfg = load_config(ROOT / CONFIGS[cfg_name])
-    cells = int(np.prod(cfg.grid.cell_shape))
-    cfg = replace(cfg, t_end=(steps + 0.5) * cfg.dt)
-    orc.run(cfg, n_steps=1)                  # warm the allocator
-    t0 = time.perf_counter()
-    orc.run(cfg, n_steps=steps)
-    dt = time.perf_counter() - t0
-    return cells * steps / dt / 1e9, dt, cells
+    cfg = load_config(ROOT / CONFIGS[cfg_name], lazy=True)
+    planes = max(2, min(planes, cfg.grid.nx))
+    sub = slab_sample_config(cfg, 0, planes)
+    cells = int(np.prod(sub.grid.cell_shape))
+    secs = _oracle_steps(sub, 1, steps)
+    return cells * steps / secs / 1e9, secs, cells
 
 
-def _replica_worker(cfg_name, steps, barrier, out):
-    """One replica of the reference arm: warm, wait for the others, time."""
-    from dataclasses import replace
-
-    from oracle import magphon_oracle as orc
+def _replica_worker(cfg_name, x0, x1, warm, steps, barrier, out):
+    """One replica of the reference arm: its x-slab of the bench config."""
     from paper_2510_22221_b200.config import load_config
-    cfg = load_config(ROOT / CONFIGS[cfg_name])
-    cfg = replace(cfg, t_end=(steps + 0.5) * cfg.dt)
-    orc.run(cfg, n_steps=1)                  # warm the allocator
+    cfg = slab_sample_config(load_config(ROOT / CONFIGS[cfg_name], lazy=True), x0, x1)
+    cfg.materials.Ms                          # dense maps before the start line
     barrier.wait()
-    t0 = time.perf_counter()
-    orc.run(cfg, n_steps=steps)
-    out.put(time.perf_counter() - t0)
+    out.put(_oracle_steps(cfg, warm, steps))
 
 
-def cpu_replicas(cfg_name: str, steps: int, procs: int):
-    """The reference's own host parallelism (sim.sweep's process pool,
-    reference sim.py:243-260): `procs` independent single-threaded runs of the
-    numpy oracle at once, one per host core.  Returns (aggregate
-    Gcell-updates/s, slowest replica's seconds, cells per replica)."""
+def cpu_slab_replicas(cfg_name: str, slabs, warm: int, steps: int):
+    """The reference's CPU path on all host cores at once: one single-threaded
+    oracle process per x-slab (the reference's numpy ufuncs are single
+    threaded; its own parallelism is a process pool, sim.py:243-260).
+    Returns (aggregate Gcell-updates/s, slowest replica's seconds, cells)."""
     import multiprocessing as mp
 
     from paper_2510_22221_b200.config import load_config
-    cells = int(np.prod(load_config(ROOT / CONFIGS[cfg_name]).grid.cell_shape))
+    g = load_config(ROOT / CONFIGS[cfg_name], lazy=True).grid
+    cells = sum(x1 - x0 for x0, x1 in slabs) * g.ny * g.nz
     ctx = mp.get_context("fork")
-    barrier = ctx.Barrier(procs)
+    barrier = ctx.Barrier(len(slabs))
     out = ctx.Queue()
-    ps = [ctx.Process(target=_replica_worker, args=(cfg_name, steps, barrier, out))
-          for _ in range(procs)]
+    ps = [ctx.Process(target=_replica_worker, args=(cfg_name, x0, x1, warm, steps, barrier, out))
+          for x0, x1 in slabs]
     for p in ps:
         p.start()
     secs = [out.get() for _ in ps]
     for p in ps:
         p.join()
     worst = max(secs)
-    return cells * steps * procs / worst / 1e9, worst, cells
+    return cells * steps / worst / 1e9, worst, cells
 
 
-def host_cores_for_replicas(cfg_name: str) -> int:
-    """All usable host cores, bounded by memory (~300 B per cell per replica,
-    half of the available RAM)."""
-    from paper_2510_22221_b200.config import load_config
-    cores = len(os.sched_getaffinity(0))
-    cells = int(np.prod(load_config(ROOT / CONFIGS[cfg_name]).grid.cell_shape))
+def reference_slabs(nx: int, ny: int, nz: int, cores: int, max_planes: int | None = None):
+    """x-slabs of [0, nx) for `cores` replicas, at most ~300 B/cell of half the
+    available host memory in total (the oracle's dense arrays)."""
     try:
         import psutil
         avail = psutil.virtual_memory().available
     except ImportError:
         avail = 16 << 30
-    return max(1, min(cores, int(0.5 * avail // (300 * cells))))
+    budget = int(0.5 * avail // (300 * ny * nz))           # planes that fit
+    planes = min(nx, budget)
+    if max_planes is not None:
+        planes = min(planes, max_planes * cores)
+    cores = max(1, min(cores, planes // 2))
+    per = max(2, planes // cores)
+    return [(r * per, (r + 1) * per) for r in range(cores)]
 
 
 def run_reference(args) -> None:
     """Reference arm: the reference's CPU path (the numpy oracle port; the
-    reference package itself cannot travel to the GPU box) on all usable host
-    cores as independent replicas -- the reference's own parallel mode -- each
-    step one step of the bounded sample on every replica."""
+    reference package cannot travel to the GPU box) on all usable host cores,
+    on the GPU arm's own workload: the bench config's x-planes split into one
+    slab per core (the whole grid when host memory allows), every replica
+    stepping its slab concurrently.  Under torchrun only rank 0 runs."""
     os.environ.setdefault("OMP_NUM_THREADS", "1")
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    sample = args.cpu_sample
-    procs = host_cores_for_replicas(sample)
-    # warm-up: one step on every replica; it also sizes the sample so that the
-    # K timed steps stay within ~2.5 minutes (else the 64^3 C1 sample)
-    _, warm_s, _ = cpu_replicas(sample, 1, procs)
-    if warm_s * args.steps > 150.0 and sample != "c1":
-        sample = "c1"
-        procs = host_cores_for_replicas(sample)
-        cpu_replicas(sample, 1, procs)
-    steps = args.steps
-    v, secs, cells = cpu_replicas(sample, steps, procs)
+    from paper_2510_22221_b200.config import load_config
+    cfg = load_config(ROOT / CONFIGS[args.config], lazy=True)
+    g = cfg.grid
+    cores = len(os.sched_getaffinity(0))
+    slabs = reference_slabs(g.nx, g.ny, g.nz, cores, args.ref_planes)
+    # one untimed step sizes the sample so that W + K steps stay within ~3 min
+    _, one, _ = cpu_slab_replicas(args.config, slabs, 0, 1)
+    budget = 180.0 / max(1, args.steps + args.warmup)
+    while one > budget and slabs[0][1] - slabs[0][0] > 2:
+        per = max(2, (slabs[0][1] - slabs[0][0]) // 2)
+        slabs = [(r * per, (r + 1) * per) for r in range(len(slabs))]
+        one /= 2.0
+    v, secs, cells = cpu_slab_replicas(args.config, slabs, args.warmup, args.steps)
+    world = max(1, args.gpus)
+    total_cells = int(np.prod(g.cell_shape)) * (world if args.scaling == "weak" else 1)
     line = {
         "metric": METRIC, "value": v, "unit": "Gcell-updates/s",
-        "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
-        "ms_per_step": secs / steps * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "impl": "reference",
-        "config": {"workload": f"{args.config} (timed on a bounded sample: {procs} "
-                               f"replicas of {sample}, {cells} cells each)",
-                   "sample_config": sample, "replicas": procs},
-        "cpu_baseline": {"value": v, "unit": "Gcell-updates/s", "cores": procs,
-                         "kind": "port",
-                         "sample": f"numpy oracle (restatement of magphon.sim.run, one "
-                                   f"thread per replica like the reference), {procs} "
-                                   f"concurrent replicas of {sample} ({cells} cells) x "
-                                   f"{steps} steps, slowest replica {secs:.1f} s"},
+        "config": workload_config(args, cfg, world, total_cells),
+        "cpu_baseline": {
+            "value": v, "unit": "Gcell-updates/s", "cores": len(slabs), "kind": "port",
+            "sample": f"numpy oracle (restatement of magphon.sim.run, one thread per "
+                      f"process like the reference) on {len(slabs)} host cores at once, "
+                      f"each stepping an x-slab of {slabs[0][1] - slabs[0][0]} planes of "
+                      f"{args.config.upper()} ({cells} of its {int(np.prod(g.cell_shape))} "
+                      f"cells per step), {args.warmup} + {args.steps} steps, slowest "
+                      f"replica {secs:.1f} s; per-cell CPU cost does not depend on N"},
         "e2e": {"value": v, "unit": "Gcell-updates/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
+
+
+def workload_config(args, cfg, world: int, total_cells: int) -> dict:
+    """The `config` object of the JSON line (identical in both arms)."""
+    g = cfg.grid
+    cells = int(np.prod(g.cell_shape))
+    per_gpu = cells if args.scaling == "weak" else cells // max(1, world)
+    return {"workload": f"{args.config.upper()} {'x'.join(map(str, g.cell_shape))} "
+                        + ("cells per GPU" if args.scaling == "weak" else
+                           f"cells split over {world} GPU(s)")
+                        + f", {DESCRIPTIONS[args.config]}, fp64",
+            "config_file": CONFIGS[args.config], "cells_per_gpu": per_gpu,
+            "cells_total": total_cells,
+            "magnetic_fraction": cfg.materials.magnetic_count() / cells,
+            "parallelism": f"x-slab x{world}" if world > 1 else "single GPU",
+            "l2": "state (2 x 6 fp64 fields) >> 126 MB L2; no flush needed",
+            "kernel_variant": args.variant,
+            "initial_state": args.init}
+
+
+def _free_port() -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def self_launch(nproc: int) -> int:
+    """`python bench.py --gpus N` without torchrun: re-run this command as N
+    ranks under torch.distributed.run (one process per GPU, rendezvous on
+    127.0.0.1), the launch the multi-GPU driver uses."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1",
+           f"--master-port={_free_port()}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    print(f"[bench] launching {nproc} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd, cwd=str(ROOT))
+
+
+def layout_only(args, world: int, rank: int) -> None:
+    """(test hook) build this rank's slab exactly as the timed run would and
+    record it as JSON in args.layout_only; no device work, gloo plumbing."""
+    import torch.distributed as dist
+
+    from paper_2510_22221_b200.config import load_config
+    dist.init_process_group("gloo")
+    cfg = load_config(ROOT / CONFIGS[args.config], lazy=True)
+    keys = list(dict.fromkeys((p[0], (p[1], p[2], p[3])) for p in cfg.probes))
+    dev, cells = slab_run(cfg, keys, world, rank, 0, args, nccl=False)
+    sl = dev.slab
+    rec = {"rank": rank, "world": world, "env_world": int(os.environ["WORLD_SIZE"]),
+           "x_lo": sl.x_lo, "x_hi": sl.x_hi, "nranks": sl.nranks, "cells": cells,
+           "grid": list(dev.grid.cell_shape)}
+    Path(args.layout_only, f"rank{rank}.json").write_text(json.dumps(rec))
+    dist.barrier()
+    dist.destroy_process_group()
 
 
 def main() -> None:
@@ -310,18 +404,33 @@ def main() -> None:
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--variant", type=int, default=0)
-    ap.add_argument("--cpu-sample", default="c2")
-    ap.add_argument("--cpu-steps", type=int, default=15)
+    ap.add_argument("--cpu-planes", type=int, default=32,
+                    help="x-planes of the bench config in the 1-core cpu_baseline sample")
+    ap.add_argument("--cpu-steps", type=int, default=8)
+    ap.add_argument("--ref-planes", type=int, default=None,
+                    help="reference arm: at most this many x-planes per host core")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=0)
     ap.add_argument("--init", default="random", choices=["random", "zero"])
     ap.add_argument("--scaling", default=None, choices=["weak", "strong"],
                     help="multi-GPU mode (default: weak for c1-c4, strong for c5)")
+    ap.add_argument("--layout-only", default=None, help=argparse.SUPPRESS)
     args = ap.parse_args()
     if args.scaling is None:
         args.scaling = "strong" if args.config == "c5" else "weak"
     if args.impl == "reference":
         run_reference(args)
+        return
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(self_launch(args.gpus))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch "
+                         f"with --nproc-per-node {args.gpus} or without torchrun")
+    if args.layout_only:
+        layout_only(args, world, rank)
         return
 
     import torch
@@ -330,9 +439,6 @@ def main() -> None:
     from paper_2510_22221_b200.config import load_config
     from paper_2510_22221_b200.grid import initial_magnetization
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
@@ -438,33 +544,31 @@ def main() -> None:
     tp = ROOT / "profiles" / "traffic.json"
     if tp.exists() and args.config == "c4" and world == 1:   # captured on C4, 1 GPU
         traffic = json.loads(tp.read_text()).get(kname)
+    comm = dev.comm_info()
+    if world > 1:
+        gathered = [None] * world
+        torch.distributed.all_gather_object(gathered, comm)
+        comm = {"nranks_per_comm": sorted({c["nranks"] for c in gathered}),
+                "ranks": [c["rank"] for c in gathered],
+                "nccl_version": comm["nccl_version"]}
     if rank != 0:
         dev.close()
         return
     cpu = None
     if not args.no_cpu:
-        rate, secs, ccells = cpu_oracle_sample(args.cpu_sample, args.cpu_steps)
+        rate, secs, ccells = cpu_oracle_sample(args.config, args.cpu_planes, args.cpu_steps)
         cpu = {"value": rate, "unit": "Gcell-updates/s", "cores": 1, "kind": "port",
                "sample": f"numpy oracle (restatement of magphon.sim.run, single "
-                         f"thread like the reference) on {args.cpu_sample} "
-                         f"({ccells} cells) x {args.cpu_steps} steps = {secs:.1f} s"}
+                         f"thread like the reference) on the first {args.cpu_planes} "
+                         f"x-planes of {args.config.upper()} ({ccells} cells) x "
+                         f"{args.cpu_steps} steps = {secs:.1f} s"}
     line = {
         "metric": METRIC, "value": value, "unit": "Gcell-updates/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": f"{args.config.upper()} {'x'.join(map(str, cfg.grid.cell_shape))} "
-                               + ("cells per GPU" if args.scaling == "weak" else
-                                  f"cells split over {world} GPU(s)")
-                               + f", {DESCRIPTIONS[args.config]}, fp64",
-                   "config_file": CONFIGS[args.config], "cells_per_gpu": rank_cells,
-                   "cells_total": total_cells,
-                   "magnetic_fraction": f_mag,
-                   "parallelism": f"x-slab x{world}" if world > 1 else "single GPU",
-                   "l2": "state (2 x 6 fp64 fields) >> 126 MB L2; no flush needed",
-                   "kernel_variant": args.variant,
-                   "initial_state": args.init},
+        "config": workload_config(args, cfg, world, total_cells),
         "e2e": {"value": e2e, "unit": "Gcell-updates/s",
                 "h2d_bytes_per_step": 8, "d2h_bytes_per_step": 8 * len(dev.probes) + 4,
                 "api": "mpb_run (pinned host source values in, pinned host probes + r* out)"},
@@ -479,6 +583,7 @@ def main() -> None:
         "cpu_baseline": cpu,
         "clocks": clk.summary(t_wall0, t_wall1),
         "gpu_launches": launches,
+        "ranks": comm,
     }
     print(json.dumps(line))
     dev.close()

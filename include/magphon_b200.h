@@ -207,6 +207,13 @@ MPB_API int mpb_total_energy(mpb_handle* h, double* out);
 /* Device bytes held by the handle. */
 MPB_API int64_t mpb_device_bytes(mpb_handle* h);
 
+/* Rank layout of the handle as its NCCL communicator reports it
+ * (ncclCommCount / ncclCommUserRank; single rank or in-process group: the
+ * setup values) and the NCCL version the library runs against.  Lets a
+ * multi-GPU driver prove how many ranks actually joined the exchange. */
+MPB_API int mpb_comm_info(mpb_handle* h, int32_t* nranks, int32_t* rank,
+                          int32_t* nccl_version);
+
 #ifdef __cplusplus
 }
 #endif

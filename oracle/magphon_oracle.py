@@ -24,6 +24,7 @@ works -- the reference's own objects and the product's mirror alike.
 from __future__ import annotations
 
 import math
+import time
 
 import numpy as np
 
@@ -313,10 +314,12 @@ def _faces(bnd):
     return {f: getattr(bnd, f) for f in ("x0", "x1", "y0", "y1", "z0", "z1")}
 
 
-def run(config, bias=None, resume=None, n_steps=None, record_first=False):
+def run(config, bias=None, resume=None, n_steps=None, record_first=False, marks=None):
     """Restatement of ``sim.run``; returns a plain dict.
 
-    ``n_steps`` (oracle-only) truncates the run for bounded CPU baselines.
+    ``n_steps`` (oracle-only) truncates the run for bounded CPU baselines;
+    ``marks`` (a list) receives ``time.perf_counter()`` at the start of every
+    step and once after the last, so a baseline can time the steps alone.
     """
     g = config.grid
     n = (g.nx, g.ny, g.nz)
@@ -355,6 +358,8 @@ def run(config, bias=None, resume=None, n_steps=None, record_first=False):
         iters = list(resume["iterations"])
     tol, max_iters = config.llg_params.tol, config.llg_params.max_iters
     for step in range(start, stop):
+        if marks is not None:
+            marks.append(time.perf_counter())
         cE = curl_e(lat, d)
         for c in range(3):
             m = masks[c]
@@ -388,6 +393,8 @@ def run(config, bias=None, resume=None, n_steps=None, record_first=False):
                 lat.E[c][i, j, k] += p * v
         for (comp, loc), buf in probes.items():
             buf.append(lat.sample(comp, *loc))
+    if marks is not None:
+        marks.append(time.perf_counter())
     out = {
         "fields": lat.state(),
         "probes": {k: np.asarray(v) for k, v in probes.items()},

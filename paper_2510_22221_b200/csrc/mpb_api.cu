@@ -343,13 +343,14 @@ int phase_fixup_single(mpb_handle* h, int pa, cudaStream_t s, int64_t& launches)
     cfg.gridDim = dim3(h->fixup_blocks);
     cfg.blockDim = dim3(256);
     cfg.stream = s;
-    cudaLaunchAttribute attr[2];
+    // cooperative only: programmatic serialization could place the grid's
+    // blocks while k_llg_local still holds SMs, and co-residency of every
+    // block is what grid.sync() needs
+    cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
-    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = h->pdl ? 2 : 1;
+    cfg.numAttrs = 1;
     MagScratch scr{h->scratch};
     CU(cudaLaunchKernelEx(&cfg, k_llg_fixup, g, b, (const mpb_material*)h->mats, ids_view(h),
                           (const int2*)h->magcells, h->nmag, scr, h->st));
@@ -712,6 +713,223 @@ int launch_line(mpb_handle* h, int64_t nsteps) {
 
 }  // namespace
 
+namespace {
+// The body of mpb_create after the handle exists (errors return; the caller
+// destroys the partially built handle).
+int create_body(const mpb_setup* su, mpb_handle* h, int nranks, int x_lo, int x_hi) {
+    const int nx = su->n[0], ny = su->n[1], nz = su->n[2];
+    h->device = su->device;
+    h->variant = su->kernel_variant;
+    h->graph_steps = su->graph_steps > 0 ? su->graph_steps : kDefaultGraphSteps;
+    if (nranks > 1) h->graph_steps = 1;   // NCCL steps are enqueued eagerly
+    h->nranks = nranks;
+    h->rank = nranks == 1 ? 0 : su->rank;
+    CU(cudaSetDevice(h->device));
+    CU(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    if (nranks > 1) {
+        CU(cudaStreamCreateWithFlags(&h->comm_stream, cudaStreamNonBlocking));
+        CU(cudaEventCreateWithFlags(&h->ev_post, cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&h->ev_exch, cudaEventDisableTiming));
+        const char* e = getenv("MPB_OVERLAP");
+        h->overlap = su->kernel_variant != 1 && !(e && atoi(e) == 0);
+    }
+
+    Geom& g = h->g;
+    int64_t F[3];
+    for (int a = 0; a < 3; ++a) {
+        g.n[a] = su->n[a];
+        g.F[a] = su->n[a] > 1 ? su->n[a] + 1 : 1;
+        g.act[a] = su->n[a] > 1;
+        g.d[a] = su->d[a];
+        F[a] = g.F[a];
+    }
+    g.FyFz = (int)(F[1] * F[2]);
+    g.PP = (F[1] * F[2] + 31) / 32 * 32;
+    if ((uint64_t)F[0] * (uint64_t)g.PP >= (1ull << 32)) { return fail_msg(MPB_EINVAL, "grid too large for 32-bit element offsets");
+    }
+    g.coef_h = su->coef_h;
+    g.max_iters = su->llg_max_iters;
+    g.tol = su->llg_tol;
+    g.zin = su->kernel_variant == 1 ? 0 : 1;
+    if (const char* e = getenv("MPB_WALLS"))        // "face": one x/y wall launch per face
+        h->wall_per_face = !strcmp(e, "face");
+    if (const char* e = getenv("MPB_PDL")) h->pdl = strcmp(e, "0") != 0;
+    if (const char* e = getenv("MPB_ZWALL"))        // "kernel": separate z-wall launches
+        if (!strcmp(e, "kernel")) g.zin = 0;
+    g.c0 = x_lo;
+    g.c1 = x_hi == nx ? (int)F[0] : x_hi;
+    h->lo = std::max(0, g.c0 - 1);
+    h->hi = std::min((int)F[0], g.c1 + 1);
+    h->clo = std::max(0, x_lo - 1);
+    h->chi = std::min(nx, x_hi + 1);
+    for (int f = 0; f < 6; ++f) {
+        g.faces[f] = su->faces[f];
+        bool act = g.act[f >> 1] && su->faces[f] != MPB_FACE_PMC;
+        if (f == 0 && g.c0 != 0) act = false;            // x walls on the end ranks
+        if (f == 1 && g.c1 != (int)F[0]) act = false;
+        h->faces_active[f] = act;
+    }
+    h->nloc = (int64_t)(h->hi - h->lo) * g.PP;
+    h->nmat_table = MPB_MAX_MATERIALS;
+
+    // material table renumbered so that magnetic materials carry bit 7 of
+    // the id (the sweep tests magnetism without a table lookup)
+    std::vector<int> remap((size_t)su->n_materials);
+    std::vector<mpb_material> table(MPB_MAX_MATERIALS);
+    memset(table.data(), 0, sizeof(mpb_material) * table.size());
+    {
+        int nm = 0, mm = 0;
+        for (int q = 0; q < su->n_materials; ++q) {
+            const int id = su->materials[q].magnetic ? 128 + mm++ : nm++;
+            if (nm > 128 || mm > 128) { return fail_msg(MPB_EINVAL, "at most 128 magnetic and 128 non-magnetic materials");
+            }
+            remap[(size_t)q] = id;
+            table[(size_t)id] = su->materials[q];
+        }
+    }
+    // material ids on the local field planes, edge-padded (em.py:248-252);
+    // magnetic cells of planes [lo, c1) (owned + the low ghost plane)
+    std::vector<uint8_t> ids((size_t)h->nloc, 0);
+    std::vector<int2> cells;
+    std::vector<unsigned char> owned;
+    int mx0 = nx, mx1 = 0;
+    for (int i = h->lo; i < h->hi; ++i)
+        for (int j = 0; j < F[1]; ++j)
+            for (int k = 0; k < F[2]; ++k) {
+                const int ci = std::min(i, nx - 1), cj = std::min(j, ny - 1),
+                          ck = std::min(k, nz - 1);
+                const uint8_t id0 =
+                    su->cell_material[((size_t)(ci - h->clo) * ny + cj) * nz + ck];
+                if (id0 >= su->n_materials) { return fail_msg(MPB_EINVAL, "material id %d out of range", id0);
+                }
+                const uint8_t id = (uint8_t)remap[id0];
+                const int64_t f = (int64_t)j * F[2] + k;
+                ids[(size_t)((i - h->lo) * g.PP + f)] = id;
+                if (i < nx && i < g.c1 && j < ny && k < nz && table[id].magnetic) {
+                    cells.push_back(make_int2(i, (int)f));
+                    owned.push_back(i >= g.c0 ? 1 : 0);
+                    mx0 = std::min(mx0, i);
+                    mx1 = std::max(mx1, i + 1);
+                }
+            }
+    h->nmag = (int)cells.size();
+    for (unsigned char o : owned) h->nmag_owned += o;
+    h->any_magnetic = nranks == 1 ? (h->nmag > 0) : (su->any_magnetic != 0);
+    if (h->nmag == 0) { mx0 = 0; mx1 = 0; }
+    g.mx0 = mx0;
+    g.mx1 = mx1;
+    h->mplanes = mx1 - mx0;
+
+    int rc = MPB_OK;
+    auto chk = [&](int r) { if (r && !rc) rc = r; };
+    for (int p = 0; p < 2; ++p)
+        for (int c = 0; c < 3; ++c) {
+            chk(dev_alloc(h, &h->E[p][c], (size_t)h->nloc));
+            chk(dev_alloc(h, &h->H[p][c], (size_t)h->nloc));
+            chk(dev_alloc(h, &h->M[p][c], (size_t)(h->mplanes * g.PP)));
+        }
+    chk(dev_alloc(h, &h->ids, (size_t)h->nloc));
+    chk(dev_alloc(h, &h->mats, (size_t)MPB_MAX_MATERIALS));
+    chk(dev_alloc(h, &h->magcells, (size_t)h->nmag));
+    chk(dev_alloc(h, &h->magowned, (size_t)h->nmag));
+    chk(dev_alloc(h, &h->scratch, (size_t)h->nmag * 12));
+    chk(dev_alloc(h, &h->st, 1));
+    if (rc) return rc;
+    CU(cudaMemcpy(h->ids, ids.data(), ids.size(), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(h->mats, table.data(), sizeof(mpb_material) * table.size(),
+                  cudaMemcpyHostToDevice));
+    if (h->nmag) {
+        CU(cudaMemcpy(h->magcells, cells.data(), sizeof(int2) * cells.size(),
+                      cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(h->magowned, owned.data(), owned.size(), cudaMemcpyHostToDevice));
+    }
+
+    // cooperative fixup grid (single rank): co-resident blocks only
+    if (h->nmag && nranks == 1) {
+        int per_sm = 0, sms = 0;
+        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_llg_fixup, 256, 0));
+        CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
+        const int need = (h->nmag + 255) / 256;
+        h->fixup_blocks = std::max(1, std::min(need, per_sm * sms));
+    }
+    {   // reciprocals of the spacings for the exact-division fast path
+        double* dr = nullptr;
+        CU(cudaMallocAsync(&dr, 3 * sizeof(double), h->stream));
+        k_recips<<<1, 1, 0, h->stream>>>(g.d[0], g.d[1], g.d[2], dr);
+        CU(cudaGetLastError());
+        CU(cudaMemcpyAsync(g.rd, dr, 3 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+        CU(cudaFreeAsync(dr, h->stream));
+        CU(cudaStreamSynchronize(h->stream));
+    }
+    if (h->variant != 1) {
+        rc = prepare_fused(h, g);
+        if (rc) return rc;
+    }
+    {   // lines along z that fit in one CTA's shared memory run in k_line
+        const char* e = getenv("MPB_LINE");
+        const bool want = !(e && atoi(e) == 0);
+        const size_t need = ((size_t)9 * g.F[2] + 3 * (size_t)h->nmat_table) * sizeof(double) +
+                            (size_t)g.F[2] + 16;
+        int optin = 0;
+        CU(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
+        if (want && h->nranks == 1 && h->variant == 0 && g.n[0] == 1 && g.n[1] == 1 &&
+            g.act[2] && g.n[2] >= 2 && h->nmag <= kLineThreads &&
+            need + 1024 <= (size_t)optin) {
+            h->line = true;
+            h->line_smem = need;
+            CU(cudaFuncSetAttribute(k_line, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)need));
+        }
+    }
+
+    // source (em.py:276-282): only the owning rank injects
+    for (int a = 0; a < 3; ++a) {
+        if (su->src_loc[a] < 0 || su->src_loc[a] >= g.F[a]) { return fail_msg(MPB_EINVAL, "source location out of range");
+        }
+        h->src.pol[a] = su->src_pol[a];
+    }
+    if (su->src_loc[0] < g.c0 || su->src_loc[0] >= g.c1)
+        h->src.pol[0] = h->src.pol[1] = h->src.pol[2] = 0.0;
+    h->src.off = su->src_loc[0] * g.PP + (int64_t)su->src_loc[1] * F[2] + su->src_loc[2];
+
+    // probes
+    h->nprobes = su->n_probes;
+    h->probe_comp.assign(su->probe_comp, su->probe_comp + su->n_probes);
+    h->probe_loc.assign(su->probe_loc, su->probe_loc + 3 * su->n_probes);
+    for (int p = 0; p < h->nprobes; ++p) {
+        const int comp = h->probe_comp[p];
+        const int* L = &h->probe_loc[3 * p];
+        const int* lim = comp >= MPB_COMP_MX ? g.n : g.F;
+        if (comp < 0 || comp > 8) { return fail_msg(MPB_EINVAL, "bad probe component"); }
+        for (int a = 0; a < 3; ++a)
+            if (L[a] < 0 || L[a] >= lim[a]) { return fail_msg(MPB_EINVAL, "probe %d outside grid", p);
+            }
+    }
+    chk(dev_alloc(h, &h->probes, (size_t)std::max(1, h->nprobes)));
+    if (h->line) chk(dev_alloc(h, &h->lprobes, (size_t)std::max(1, h->nprobes)));
+    h->hostM.clear();
+    if (rc) return rc;
+    bool zero_id = true;
+    for (int q = 0; q < 128; ++q) zero_id = zero_id && su->nccl_id[q] == 0;
+    if (nranks > 1 && !zero_id) {   // all-zero id: in-process group (mpb_group_run)
+        ncclUniqueId id;
+        memcpy(&id, su->nccl_id, sizeof id);
+        ncclResult_t r = ncclCommInitRank(&h->comm, nranks, id, h->rank);
+        if (r != ncclSuccess) { return fail_msg(MPB_ECUDA, "ncclCommInitRank failed: %s", ncclGetErrorString(r));
+        }
+        if (h->overlap) {   // collective over the ranks, same order everywhere
+            r = ncclCommSplit(h->comm, 0, h->rank, &h->comm_x, nullptr);
+            if (r != ncclSuccess) { return fail_msg(MPB_ECUDA, "ncclCommSplit failed: %s", ncclGetErrorString(r));
+            }
+        }
+    }
+    rc = reset_state(h);
+    if (rc) return rc;
+    return MPB_OK;
+}
+
+}  // namespace
+
 // ---------------------------------------------------------------------------
 // ABI
 // ---------------------------------------------------------------------------
@@ -770,226 +988,8 @@ int mpb_create(const mpb_setup* su, mpb_handle** out) {
             return fail_msg(MPB_EINVAL, "multi-rank runs use the fused sweep (variant 0)");
     }
     auto* h = new mpb_handle();
-    h->device = su->device;
-    h->variant = su->kernel_variant;
-    h->graph_steps = su->graph_steps > 0 ? su->graph_steps : kDefaultGraphSteps;
-    if (nranks > 1) h->graph_steps = 1;   // NCCL steps are enqueued eagerly
-    h->nranks = nranks;
-    h->rank = nranks == 1 ? 0 : su->rank;
-    CU(cudaSetDevice(h->device));
-    CU(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
-    if (nranks > 1) {
-        CU(cudaStreamCreateWithFlags(&h->comm_stream, cudaStreamNonBlocking));
-        CU(cudaEventCreateWithFlags(&h->ev_post, cudaEventDisableTiming));
-        CU(cudaEventCreateWithFlags(&h->ev_exch, cudaEventDisableTiming));
-        const char* e = getenv("MPB_OVERLAP");
-        h->overlap = su->kernel_variant != 1 && !(e && atoi(e) == 0);
-    }
-
-    Geom& g = h->g;
-    int64_t F[3];
-    for (int a = 0; a < 3; ++a) {
-        g.n[a] = su->n[a];
-        g.F[a] = su->n[a] > 1 ? su->n[a] + 1 : 1;
-        g.act[a] = su->n[a] > 1;
-        g.d[a] = su->d[a];
-        F[a] = g.F[a];
-    }
-    g.FyFz = (int)(F[1] * F[2]);
-    g.PP = (F[1] * F[2] + 31) / 32 * 32;
-    if ((uint64_t)F[0] * (uint64_t)g.PP >= (1ull << 32)) {
-        mpb_destroy(h);
-        return fail_msg(MPB_EINVAL, "grid too large for 32-bit element offsets");
-    }
-    g.coef_h = su->coef_h;
-    g.max_iters = su->llg_max_iters;
-    g.tol = su->llg_tol;
-    g.zin = su->kernel_variant == 1 ? 0 : 1;
-    if (const char* e = getenv("MPB_WALLS"))        // "face": one x/y wall launch per face
-        h->wall_per_face = !strcmp(e, "face");
-    if (const char* e = getenv("MPB_PDL")) h->pdl = strcmp(e, "0") != 0;
-    if (const char* e = getenv("MPB_ZWALL"))        // "kernel": separate z-wall launches
-        if (!strcmp(e, "kernel")) g.zin = 0;
-    g.c0 = x_lo;
-    g.c1 = x_hi == nx ? (int)F[0] : x_hi;
-    h->lo = std::max(0, g.c0 - 1);
-    h->hi = std::min((int)F[0], g.c1 + 1);
-    h->clo = std::max(0, x_lo - 1);
-    h->chi = std::min(nx, x_hi + 1);
-    for (int f = 0; f < 6; ++f) {
-        g.faces[f] = su->faces[f];
-        bool act = g.act[f >> 1] && su->faces[f] != MPB_FACE_PMC;
-        if (f == 0 && g.c0 != 0) act = false;            // x walls on the end ranks
-        if (f == 1 && g.c1 != (int)F[0]) act = false;
-        h->faces_active[f] = act;
-    }
-    h->nloc = (int64_t)(h->hi - h->lo) * g.PP;
-    h->nmat_table = MPB_MAX_MATERIALS;
-
-    // material table renumbered so that magnetic materials carry bit 7 of
-    // the id (the sweep tests magnetism without a table lookup)
-    std::vector<int> remap((size_t)su->n_materials);
-    std::vector<mpb_material> table(MPB_MAX_MATERIALS);
-    memset(table.data(), 0, sizeof(mpb_material) * table.size());
-    {
-        int nm = 0, mm = 0;
-        for (int q = 0; q < su->n_materials; ++q) {
-            const int id = su->materials[q].magnetic ? 128 + mm++ : nm++;
-            if (nm > 128 || mm > 128) {
-                mpb_destroy(h);
-                return fail_msg(MPB_EINVAL, "at most 128 magnetic and 128 non-magnetic materials");
-            }
-            remap[(size_t)q] = id;
-            table[(size_t)id] = su->materials[q];
-        }
-    }
-    // material ids on the local field planes, edge-padded (em.py:248-252);
-    // magnetic cells of planes [lo, c1) (owned + the low ghost plane)
-    std::vector<uint8_t> ids((size_t)h->nloc, 0);
-    std::vector<int2> cells;
-    std::vector<unsigned char> owned;
-    int mx0 = nx, mx1 = 0;
-    for (int i = h->lo; i < h->hi; ++i)
-        for (int j = 0; j < F[1]; ++j)
-            for (int k = 0; k < F[2]; ++k) {
-                const int ci = std::min(i, nx - 1), cj = std::min(j, ny - 1),
-                          ck = std::min(k, nz - 1);
-                const uint8_t id0 =
-                    su->cell_material[((size_t)(ci - h->clo) * ny + cj) * nz + ck];
-                if (id0 >= su->n_materials) {
-                    mpb_destroy(h);
-                    return fail_msg(MPB_EINVAL, "material id %d out of range", id0);
-                }
-                const uint8_t id = (uint8_t)remap[id0];
-                const int64_t f = (int64_t)j * F[2] + k;
-                ids[(size_t)((i - h->lo) * g.PP + f)] = id;
-                if (i < nx && i < g.c1 && j < ny && k < nz && table[id].magnetic) {
-                    cells.push_back(make_int2(i, (int)f));
-                    owned.push_back(i >= g.c0 ? 1 : 0);
-                    mx0 = std::min(mx0, i);
-                    mx1 = std::max(mx1, i + 1);
-                }
-            }
-    h->nmag = (int)cells.size();
-    for (unsigned char o : owned) h->nmag_owned += o;
-    h->any_magnetic = nranks == 1 ? (h->nmag > 0) : (su->any_magnetic != 0);
-    if (h->nmag == 0) { mx0 = 0; mx1 = 0; }
-    g.mx0 = mx0;
-    g.mx1 = mx1;
-    h->mplanes = mx1 - mx0;
-
-    int rc = MPB_OK;
-    auto chk = [&](int r) { if (r && !rc) rc = r; };
-    for (int p = 0; p < 2; ++p)
-        for (int c = 0; c < 3; ++c) {
-            chk(dev_alloc(h, &h->E[p][c], (size_t)h->nloc));
-            chk(dev_alloc(h, &h->H[p][c], (size_t)h->nloc));
-            chk(dev_alloc(h, &h->M[p][c], (size_t)(h->mplanes * g.PP)));
-        }
-    chk(dev_alloc(h, &h->ids, (size_t)h->nloc));
-    chk(dev_alloc(h, &h->mats, (size_t)MPB_MAX_MATERIALS));
-    chk(dev_alloc(h, &h->magcells, (size_t)h->nmag));
-    chk(dev_alloc(h, &h->magowned, (size_t)h->nmag));
-    chk(dev_alloc(h, &h->scratch, (size_t)h->nmag * 12));
-    chk(dev_alloc(h, &h->st, 1));
-    if (rc) { mpb_destroy(h); return rc; }
-    CU(cudaMemcpy(h->ids, ids.data(), ids.size(), cudaMemcpyHostToDevice));
-    CU(cudaMemcpy(h->mats, table.data(), sizeof(mpb_material) * table.size(),
-                  cudaMemcpyHostToDevice));
-    if (h->nmag) {
-        CU(cudaMemcpy(h->magcells, cells.data(), sizeof(int2) * cells.size(),
-                      cudaMemcpyHostToDevice));
-        CU(cudaMemcpy(h->magowned, owned.data(), owned.size(), cudaMemcpyHostToDevice));
-    }
-
-    // cooperative fixup grid (single rank): co-resident blocks only
-    if (h->nmag && nranks == 1) {
-        int per_sm = 0, sms = 0;
-        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_llg_fixup, 256, 0));
-        CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
-        const int need = (h->nmag + 255) / 256;
-        h->fixup_blocks = std::max(1, std::min(need, per_sm * sms));
-    }
-    {   // reciprocals of the spacings for the exact-division fast path
-        double* dr = nullptr;
-        CU(cudaMallocAsync(&dr, 3 * sizeof(double), h->stream));
-        k_recips<<<1, 1, 0, h->stream>>>(g.d[0], g.d[1], g.d[2], dr);
-        CU(cudaGetLastError());
-        CU(cudaMemcpyAsync(g.rd, dr, 3 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-        CU(cudaFreeAsync(dr, h->stream));
-        CU(cudaStreamSynchronize(h->stream));
-    }
-    if (h->variant != 1) {
-        rc = prepare_fused(h, g);
-        if (rc) { mpb_destroy(h); return rc; }
-    }
-    {   // lines along z that fit in one CTA's shared memory run in k_line
-        const char* e = getenv("MPB_LINE");
-        const bool want = !(e && atoi(e) == 0);
-        const size_t need = ((size_t)9 * g.F[2] + 3 * (size_t)h->nmat_table) * sizeof(double) +
-                            (size_t)g.F[2] + 16;
-        int optin = 0;
-        CU(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
-        if (want && h->nranks == 1 && h->variant == 0 && g.n[0] == 1 && g.n[1] == 1 &&
-            g.act[2] && g.n[2] >= 2 && h->nmag <= kLineThreads &&
-            need + 1024 <= (size_t)optin) {
-            h->line = true;
-            h->line_smem = need;
-            CU(cudaFuncSetAttribute(k_line, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)need));
-        }
-    }
-
-    // source (em.py:276-282): only the owning rank injects
-    for (int a = 0; a < 3; ++a) {
-        if (su->src_loc[a] < 0 || su->src_loc[a] >= g.F[a]) {
-            mpb_destroy(h);
-            return fail_msg(MPB_EINVAL, "source location out of range");
-        }
-        h->src.pol[a] = su->src_pol[a];
-    }
-    if (su->src_loc[0] < g.c0 || su->src_loc[0] >= g.c1)
-        h->src.pol[0] = h->src.pol[1] = h->src.pol[2] = 0.0;
-    h->src.off = su->src_loc[0] * g.PP + (int64_t)su->src_loc[1] * F[2] + su->src_loc[2];
-
-    // probes
-    h->nprobes = su->n_probes;
-    h->probe_comp.assign(su->probe_comp, su->probe_comp + su->n_probes);
-    h->probe_loc.assign(su->probe_loc, su->probe_loc + 3 * su->n_probes);
-    for (int p = 0; p < h->nprobes; ++p) {
-        const int comp = h->probe_comp[p];
-        const int* L = &h->probe_loc[3 * p];
-        const int* lim = comp >= MPB_COMP_MX ? g.n : g.F;
-        if (comp < 0 || comp > 8) { mpb_destroy(h); return fail_msg(MPB_EINVAL, "bad probe component"); }
-        for (int a = 0; a < 3; ++a)
-            if (L[a] < 0 || L[a] >= lim[a]) {
-                mpb_destroy(h);
-                return fail_msg(MPB_EINVAL, "probe %d outside grid", p);
-            }
-    }
-    chk(dev_alloc(h, &h->probes, (size_t)std::max(1, h->nprobes)));
-    if (h->line) chk(dev_alloc(h, &h->lprobes, (size_t)std::max(1, h->nprobes)));
-    h->hostM.clear();
-    if (rc) { mpb_destroy(h); return rc; }
-    bool zero_id = true;
-    for (int q = 0; q < 128; ++q) zero_id = zero_id && su->nccl_id[q] == 0;
-    if (nranks > 1 && !zero_id) {   // all-zero id: in-process group (mpb_group_run)
-        ncclUniqueId id;
-        memcpy(&id, su->nccl_id, sizeof id);
-        ncclResult_t r = ncclCommInitRank(&h->comm, nranks, id, h->rank);
-        if (r != ncclSuccess) {
-            mpb_destroy(h);
-            return fail_msg(MPB_ECUDA, "ncclCommInitRank failed: %s", ncclGetErrorString(r));
-        }
-        if (h->overlap) {   // collective over the ranks, same order everywhere
-            r = ncclCommSplit(h->comm, 0, h->rank, &h->comm_x, nullptr);
-            if (r != ncclSuccess) {
-                mpb_destroy(h);
-                return fail_msg(MPB_ECUDA, "ncclCommSplit failed: %s", ncclGetErrorString(r));
-            }
-        }
-    }
-    rc = reset_state(h);
+    // every failure past this point releases what was set up so far
+    const int rc = create_body(su, h, nranks, x_lo, x_hi);
     if (rc) { mpb_destroy(h); return rc; }
     *out = h;
     return MPB_OK;
@@ -1351,6 +1351,24 @@ int mpb_total_energy(mpb_handle* h, double* out) {
     const double mu0 = 4e-7 * 3.141592653589793;
     const double vol = g.d[0] * g.d[1] * g.d[2];
     *out = (0.5 * se + 0.5 * mu0 * sh + (-mu0) * sm) * vol;
+    return MPB_OK;
+}
+
+int mpb_comm_info(mpb_handle* h, int32_t* nranks, int32_t* rank, int32_t* nccl_version) {
+    g_err.clear();
+    if (!h || !nranks || !rank || !nccl_version) return fail_msg(MPB_EINVAL, "null argument");
+    int v = 0;
+    NC(ncclGetVersion(&v));
+    *nccl_version = v;
+    *nranks = h->nranks;
+    *rank = h->rank;
+    if (h->comm) {   // what the communicator itself reports
+        int cnt = 0, me = 0;
+        NC(ncclCommCount(h->comm, &cnt));
+        NC(ncclCommUserRank(h->comm, &me));
+        *nranks = cnt;
+        *rank = me;
+    }
     return MPB_OK;
 }
 

@@ -291,6 +291,12 @@ class DeviceRun:
         N.check(self.lib.mpb_total_energy(self.h, C.byref(out)))
         return out.value
 
+    def comm_info(self) -> dict:
+        """Ranks as the NCCL communicator reports them + the NCCL version."""
+        n, r, v = C.c_int32(), C.c_int32(), C.c_int32()
+        N.check(self.lib.mpb_comm_info(self.h, C.byref(n), C.byref(r), C.byref(v)))
+        return {"nranks": n.value, "rank": r.value, "nccl_version": v.value}
+
     def launch_count(self) -> int:
         return int(self.lib.mpb_launch_count(self.h))
 

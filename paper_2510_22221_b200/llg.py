@@ -1,6 +1,7 @@
 """Host-side types of the coupled LLG fixed point.
 
-The iteration itself runs on the GPU (``csrc/mpb_kernels.cu``); this module
+The iteration itself runs on the GPU (``csrc/mpb_sweep.cuh`` ``k_llg_local``,
+``csrc/mpb_kernels_split.cuh`` ``k_llg_fixup``); this module
 keeps the reference's public types so callers catch the same exception
 (reference ``pkg/src/magphon/llg.py:38-58``).
 """

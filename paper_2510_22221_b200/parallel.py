@@ -8,9 +8,10 @@ Partition: rank r owns cell planes ``[x_lo, x_hi)`` (balanced, >= 2 planes
 each); the last rank also owns field plane nx.  Each rank keeps one ghost
 field plane on each side: field planes ``[max(0, x_lo-1), min(F, x_hi'+1))``
 with ``x_hi' = F`` on the last rank; cell (material, M) planes
-``[max(0, x_lo-1), min(nx, x_hi+1))``.  The same functions drive the CPU
-emulation in ``tests/test_slab_emulation.py`` (gloo), which checks the plan
-bit for bit against the single-domain oracle.
+``[max(0, x_lo-1), min(nx, x_hi+1))``.  The same functions drive the
+per-process host tests in ``tests/test_parallel_host.py`` (gloo, 2 ranks) and
+the one-GPU rank emulation in ``tests/test_slab_gpu.py``, which checks the
+plan bit for bit against the single-domain oracle goldens.
 """
 
 from __future__ import annotations

@@ -121,33 +121,67 @@ def source_values(src: em.SourceSpec, dt: float, start: int, stop: int) -> np.nd
 
 def _device_run_args(config, keys) -> dict:
     """Validate probes/walls/source like the reference would at run time and
-    return the device-facing source and wall arguments."""
+    return the device-facing source and wall arguments.
+
+    The reference raises these errors inside its first step, in this order:
+    MUR1 on a collapsed axis (``em._capture_mur_planes``, em.py:306-321),
+    the source index (``inject_soft_source``), then each probe in config
+    order (``FieldLattice.sample``: unknown component, then index range).
+    """
     fs = config.grid.field_shape
+    b = config.boundaries
+    for face, axis in (("x0", 0), ("x1", 0), ("y0", 1), ("y1", 1), ("z0", 2), ("z1", 2)):
+        if getattr(b, face) == em.MUR1 and not config.grid.active_axes[axis]:
+            raise ValueError(f"MUR1 on collapsed axis face {face}")
     pol = config.source.polarization
     loc = config.source.location
     if any(p != 0.0 for p in pol):
         loc = _wrap_source(loc, fs)
     else:
         loc = (0, 0, 0)
-    for comp, _ in keys:
+    for comp, (i, j, k) in keys:
         if comp not in _VALID_COMPS:
             raise KeyError(f"unknown field component {comp!r}")
-    for comp, (i, j, k) in keys:
         lim = config.grid.cell_shape if comp.startswith("M") else fs
         if not all(0 <= x < n for x, n in zip((i, j, k), lim)):
             raise IndexError(f"index ({i},{j},{k}) out of range for {comp}")
-    b = config.boundaries
-    for face, axis in (("x0", 0), ("x1", 0), ("y0", 1), ("y1", 1), ("z0", 2), ("z1", 2)):
-        if getattr(b, face) == em.MUR1 and not config.grid.active_axes[axis]:
-            raise ValueError(f"MUR1 on collapsed axis face {face}")
     return {"source_loc": loc, "source_pol": pol, "boundaries": b}
 
 
-def _device_run(config, materials, keys, device: int = 0, **kw) -> DeviceRun:
-    a = _device_run_args(config, keys)
+def _unchecked_run_args(config) -> dict:
+    """Device arguments that skip the run-time checks: no source, and PEC in
+    place of MUR1 on collapsed axes.  Used only where the reference would
+    not reach those checks (no step to run) or to find out whether the LLG
+    of the first step fails before them."""
+    b = config.boundaries
+    repl = {face: em.PEC for face, axis in (("x0", 0), ("x1", 0), ("y0", 1), ("y1", 1),
+                                            ("z0", 2), ("z1", 2))
+            if getattr(b, face) == em.MUR1 and not config.grid.active_axes[axis]}
+    return {"source_loc": (0, 0, 0), "source_pol": (0.0, 0.0, 0.0),
+            "boundaries": replace(b, **repl) if repl else b}
+
+
+def _device_run(config, materials, keys, device: int = 0, *, checked: bool = True,
+                **kw) -> DeviceRun:
+    a = _device_run_args(config, keys) if checked else _unchecked_run_args(config)
     return DeviceRun(config.grid, materials, a["boundaries"], a["source_loc"],
-                     a["source_pol"], keys, config.llg_params, config.dt,
-                     device=device, **kw)
+                     a["source_pol"], keys if checked else [], config.llg_params,
+                     config.dt, device=device, **kw)
+
+
+def _raise_failure(fail, config):
+    step, res, it, kind = fail
+    if kind == 1:
+        msg = (f"fixed-point iteration diverging (residual {res:.3e} "
+               f"after {it} iterates)")
+    elif kind == 3:
+        msg = (f"fixed-point iteration: global residual non-monotone across ranks "
+               f"at iterate {it} (residual {res:.3e})")
+    else:
+        msg = (f"fixed-point iteration did not reach tol "
+               f"{config.llg_params.tol:.1e} in "
+               f"{config.llg_params.max_iters} iterates (residual {res:.3e})")
+    raise llg.StepFailure(msg, res, it, step=step)
 
 
 def run(config: SimConfig, bias: float | None = None, resume: dict | None = None,
@@ -171,7 +205,15 @@ def run(config: SimConfig, bias: float | None = None, resume: dict | None = None
             buffers[key] = list(vals)
         iters_prefix = list(resume["iterations"])
     keys = list(buffers)
-    dev = _device_run(config, materials, keys, device=device,
+    count = max(0, n_steps - start)
+    pending = None
+    try:
+        _device_run_args(config, keys)
+    except (ValueError, IndexError, KeyError) as exc:
+        # the reference raises these inside its first step, after that
+        # step's LLG; with no step left to run it never reaches them
+        pending = exc
+    dev = _device_run(config, materials, keys, device=device, checked=pending is None,
                       kernel_variant=kernel_variant)
     try:
         if resume is not None:
@@ -179,19 +221,17 @@ def run(config: SimConfig, bias: float | None = None, resume: dict | None = None
             dev.load_state({n: st[n] for n in _FIELD_NAMES}, st["M"])
         else:
             dev.load_state(None, initial_magnetization(materials))   # E = H = 0
-        count = max(0, n_steps - start)
+        if pending is not None and count > 0:
+            # one step of the unchecked run: a StepFailure of the first
+            # step's LLG wins over the error its E update would raise
+            _, _, fail = dev.run(start, np.zeros(1))
+            if fail is not None:
+                _raise_failure(fail, config)
+            raise pending
         vals = source_values(config.source, dt, start, n_steps)
         probe_rows, iters, fail = dev.run(start, vals)
         if fail is not None:
-            step, res, it, kind = fail
-            if kind == 1:
-                msg = (f"fixed-point iteration diverging (residual {res:.3e} "
-                       f"after {it} iterates)")
-            else:
-                msg = (f"fixed-point iteration did not reach tol "
-                       f"{config.llg_params.tol:.1e} in "
-                       f"{config.llg_params.max_iters} iterates (residual {res:.3e})")
-            raise llg.StepFailure(msg, res, it, step=step)
+            _raise_failure(fail, config)
         state = dev.save_state()
     finally:
         dev.close()
@@ -199,8 +239,8 @@ def run(config: SimConfig, bias: float | None = None, resume: dict | None = None
     b = 0.0 if bias is None else bias
     probes = {}
     for p, key in enumerate(keys):
-        samples = np.concatenate([np.asarray(buffers[key], dtype=np.float64),
-                                  probe_rows[:count, p]])
+        tail = probe_rows[:count, p] if count else np.zeros(0)
+        samples = np.concatenate([np.asarray(buffers[key], dtype=np.float64), tail])
         probes[key] = ProbeSeries(component=key[0], location=key[1], bias=b,
                                   dt_sample=dt, samples=samples)
     if dev.n_magnetic > 0:
