@@ -204,6 +204,12 @@ MPB_API int mpb_selftest_division(int32_t device, double d, const double* x, int
  * rounding (summation order differs), not bitwise. */
 MPB_API int mpb_total_energy(mpb_handle* h, double* out);
 
+/* Tile form the fused sweep was set up with: out = {entries per thread,
+ * threads per CTA, entries per tile, x-chunks} (zeros when the split
+ * variant or the line kernel runs).  Lets a test pin the exact kernel
+ * instantiation a benchmark times. */
+MPB_API int mpb_sweep_form(mpb_handle* h, int32_t out[4]);
+
 /* Device bytes held by the handle. */
 MPB_API int64_t mpb_device_bytes(mpb_handle* h);
 

@@ -149,6 +149,7 @@ int launch_zfix(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s);
 int zfix_launches(mpb_handle* h);
 int launch_llg_local(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s);
 const char* fused_kernel_name();
+void fused_form(mpb_handle* h, int32_t out[4]);
 }  // namespace
 
 namespace {
@@ -1373,6 +1374,13 @@ int mpb_comm_info(mpb_handle* h, int32_t* nranks, int32_t* rank, int32_t* nccl_v
 }
 
 int64_t mpb_launch_count(mpb_handle* h) { return h ? h->launches_last : 0; }
+
+int mpb_sweep_form(mpb_handle* h, int32_t out[4]) {
+    g_err.clear();
+    if (!h || !out) return fail_msg(MPB_EINVAL, "null argument");
+    fused_form(h, out);
+    return MPB_OK;
+}
 
 int64_t mpb_device_bytes(mpb_handle* h) { return h ? h->bytes : 0; }
 

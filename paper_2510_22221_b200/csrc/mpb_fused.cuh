@@ -313,4 +313,13 @@ int launch_deferred(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s)
 
 const char* fused_kernel_name() { return "k_sweep"; }
 
+// tile form of the fused sweep: {entries per thread V, CTA threads NT,
+// entries per tile T, x-chunks}; zeros for the split variant / line kernel
+void fused_form(mpb_handle* h, int32_t out[4]) {
+    FusedState* fs = fused_of(h);
+    out[0] = out[1] = out[2] = out[3] = 0;
+    if (!fs || h->line) return;
+    out[0] = fs->V; out[1] = fs->NT; out[2] = fs->sc.T; out[3] = fs->sc.nchunks;
+}
+
 }  // namespace

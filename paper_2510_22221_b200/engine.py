@@ -291,6 +291,12 @@ class DeviceRun:
         N.check(self.lib.mpb_total_energy(self.h, C.byref(out)))
         return out.value
 
+    def sweep_form(self) -> dict:
+        """Tile form of the fused sweep (V, NT, T, x-chunks)."""
+        out = (C.c_int32 * 4)()
+        N.check(self.lib.mpb_sweep_form(self.h, out))
+        return {"V": out[0], "NT": out[1], "T": out[2], "chunks": out[3]}
+
     def comm_info(self) -> dict:
         """Ranks as the NCCL communicator reports them + the NCCL version."""
         n, r, v = C.c_int32(), C.c_int32(), C.c_int32()
