@@ -112,9 +112,13 @@ typedef struct mpb_failure {
     int64_t step;           /* -1 if no failure                                */
     double residual;
     int32_t iterations;
-    int32_t kind;           /* 1 = diverging, 2 = budget exhausted,
-                               3 = multi-rank: global residual non-monotone at r*
-                                   (unsupported across ranks; reported, not guessed) */
+    int32_t kind;           /* 1 = diverging, 2 = budget exhausted (llg.py:139-148);
+                               4 = multi-rank step suspended: its global residual
+                                   went back above tol after the last local stop.
+                                   mpb_run / mpb_group_run continue such a step in
+                                   lockstep (one all-reduce per iterate) and never
+                                   return 4; only mpb_run_device + mpb_check_failure
+                                   can report it. */
 } mpb_failure;
 
 typedef struct mpb_handle mpb_handle;
@@ -203,6 +207,11 @@ MPB_API int mpb_selftest_division(int32_t device, double d, const double* x, int
  * ranks).  Deterministic fixed-order reduction; equal to the reference to
  * rounding (summation order differs), not bitwise. */
 MPB_API int mpb_total_energy(mpb_handle* h, double* out);
+
+/* Multi-rank steps whose global residual went back above tol after the
+ * last local stop and were continued in host-driven lockstep since the
+ * handle was created (see mpb_failure.kind 4). */
+MPB_API int64_t mpb_continued_steps(mpb_handle* h);
 
 /* Tile form the fused sweep was set up with: out = {entries per thread,
  * threads per CTA, entries per tile, x-chunks} (zeros when the split

@@ -134,6 +134,7 @@ struct mpb_handle {
     double timed_ms = 0.0;
     int64_t timed_launches = 0;
     int64_t launches_last = 0;
+    int64_t continued_steps = 0;   // suspended multi-rank steps continued on the host
     int64_t bytes = 0;
     void* fused = nullptr;         // FusedState (mpb_fused.cuh)
 };
@@ -431,6 +432,23 @@ int phase_post(mpb_handle* h, int pa, cudaStream_t s, int64_t& launches,
     return MPB_OK;
 }
 
+// End of a slab step: the boundary planes of the new state (set 1 - pa)
+// to the neighbours, on the comm stream overlapping the next interior sweep.
+int end_step_exchange(mpb_handle* h, int pa) {
+    int rc;
+    cudaStream_t s = h->stream;
+    if (h->overlap) {
+        CU(cudaEventRecord(h->ev_post, s));
+        CU(cudaStreamWaitEvent(h->comm_stream, h->ev_post, 0));
+        if ((rc = exchange(h, 1 - pa, h->comm_stream))) return rc;
+        CU(cudaEventRecord(h->ev_exch, h->comm_stream));
+        h->exch_pending = true;
+    } else if ((rc = exchange(h, 1 - pa, s))) {
+        return rc;
+    }
+    return MPB_OK;
+}
+
 // Enqueue one coupled step reading buffer set `pa` (single rank or NCCL).
 int enqueue_step(mpb_handle* h, int pa, bool timed) {
     const Geom& g = h->g;
@@ -477,17 +495,7 @@ int enqueue_step(mpb_handle* h, int pa, bool timed) {
     } else {
         if ((rc = phase_post(h, pa, s, launches))) return rc;
     }
-    if (h->nranks > 1) {
-        if (h->overlap) {   // on the comm stream, overlapping the next interior sweep
-            CU(cudaEventRecord(h->ev_post, s));
-            CU(cudaStreamWaitEvent(h->comm_stream, h->ev_post, 0));
-            if ((rc = exchange(h, 1 - pa, h->comm_stream))) return rc;
-            CU(cudaEventRecord(h->ev_exch, h->comm_stream));
-            h->exch_pending = true;
-        } else if ((rc = exchange(h, 1 - pa, s))) {
-            return rc;
-        }
-    }
+    if (h->nranks > 1 && (rc = end_step_exchange(h, pa))) return rc;
     h->launches_last += launches;
     CU(cudaGetLastError());
     return MPB_OK;
@@ -560,6 +568,98 @@ int drain_exchange(mpb_handle* h, cudaStream_t s) {
         CU(cudaStreamWaitEvent(s, h->ev_exch, 0));
         h->exch_pending = false;
     }
+    return MPB_OK;
+}
+
+// Host replay of llg_decide (mpb_device.cuh) on an all-reduced history.
+int host_decide(const unsigned long long* hist, int upto, int max_iters, double tol,
+                double* fres, int* fit, int* fkind) {
+    double prev = INFINITY;
+    int growth = 0;
+    for (int it = 1; it <= upto; ++it) {
+        double res;
+        memcpy(&res, &hist[it], sizeof res);
+        if (res <= tol) return it;
+        growth = (res > prev) ? growth + 1 : 0;
+        if (growth >= 3) { *fres = res; *fit = it; *fkind = 1; return 0; }
+        prev = res;
+        if (it == max_iters) { *fres = prev; *fit = max_iters; *fkind = 2; return 0; }
+    }
+    return -1;
+}
+
+// Continue a suspended multi-rank step (k_llg_decide, kMpbSuspend) exactly
+// as the reference's lockstep loop does (llg.py:131-148): every rank
+// recomputes its cells from the step-n state one iterate at a time, the
+// owned residual maxima are all-reduced after each iterate and the stop /
+// failure rule is replayed on the host until it decides.  Then the step is
+// finished as usual (deferred E, walls, source, probes, exchange).  hs are
+// the n local handles (one for NCCL, all ranks for the in-process group),
+// positioned at the suspended step's parity; the sweep's E^{n+1} of that
+// step is intact (only k_llg_decide's successors were skipped).
+int recover_suspended(mpb_handle* const* hs, int n, bool group, cudaStream_t s) {
+    mpb_handle* h0 = hs[0];
+    const Geom& g = h0->g;
+    const int pa = h0->parity;
+    int rc;
+    int64_t launches = 0;
+    if ((rc = drain_exchange(h0, s))) return rc;
+    for (int q = 0; q < n; ++q) {
+        k_suspend_clear<<<1, 256, 0, s>>>(hs[q]->st, g.max_iters);
+        const Bufs b = make_bufs(hs[q], pa);
+        if (hs[q]->nmag)
+            k_llg_cont_init<<<(hs[q]->nmag + 255) / 256, 256, 0, s>>>(
+                hs[q]->g, b, hs[q]->magcells, hs[q]->nmag, MagScratch{hs[q]->scratch});
+    }
+    CU(cudaGetLastError());
+    std::vector<unsigned long long> hist((size_t)g.max_iters + 2, 0ull);
+    int rstar = -1, fit = 0, fkind = 0;
+    double fres = 0.0;
+    StatePtrs sp{};
+    sp.n = n;
+    for (int q = 0; q < n; ++q) sp.s[q] = hs[q]->st;
+    for (int r = 1; r <= g.max_iters && rstar < 0; ++r) {
+        for (int q = 0; q < n; ++q)
+            if (hs[q]->nmag)
+                k_llg_cont_iter<<<(hs[q]->nmag + 255) / 256, 256, 0, s>>>(
+                    hs[q]->g, hs[q]->mats, ids_view(hs[q]), hs[q]->magcells,
+                    hs[q]->magowned, hs[q]->nmag, MagScratch{hs[q]->scratch}, hs[q]->st, r);
+        CU(cudaGetLastError());
+        if (group) {
+            k_group_reduce<<<1, 256, 0, s>>>(sp, g.max_iters, 1);
+        } else {
+            NC(ncclAllReduce(&h0->st->hist2[r], &h0->st->hist2[r], 1, ncclUint64, ncclMax,
+                             h0->comm, s));
+        }
+        CU(cudaMemcpyAsync(hist.data(), h0->st->hist2, sizeof(unsigned long long) * (r + 1),
+                           cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+        const int d = host_decide(hist.data(), r, g.max_iters, g.tol, &fres, &fit, &fkind);
+        if (d > 0) rstar = d;
+        else if (d == 0) rstar = 0;
+    }
+    if (rstar <= 0) {   // the reference raises StepFailure at this step
+        for (int q = 0; q < n; ++q)
+            k_set_failure<<<1, 1, 0, s>>>(hs[q]->st, fres, fit, fkind);
+        CU(cudaGetLastError());
+        return MPB_OK;   // the caller reads the failure record
+    }
+    for (int q = 0; q < n; ++q) {
+        const Bufs b = make_bufs(hs[q], pa);
+        k_llg_cont_write<<<(std::max(hs[q]->nmag, 1) + 255) / 256, 256, 0, s>>>(
+            hs[q]->g, b, hs[q]->magcells, hs[q]->magowned, hs[q]->nmag,
+            MagScratch{hs[q]->scratch}, hs[q]->st, rstar);
+    }
+    CU(cudaGetLastError());
+    for (int q = 0; q < n; ++q)
+        if ((rc = phase_post(hs[q], pa, s, launches))) return rc;
+    if (group) {
+        if ((rc = exchange_group(hs, n, 1 - pa, s))) return rc;
+    } else if ((rc = end_step_exchange(h0, pa))) {
+        return rc;
+    }
+    for (int q = 0; q < n; ++q) ++hs[q]->continued_steps;
+    CU(cudaGetLastError());
     return MPB_OK;
 }
 
@@ -1169,9 +1269,25 @@ int mpb_run(mpb_handle* h, int64_t n0, int64_t nsteps, const double* src_vals,
         CU(cudaMemcpyAsync(h->d_src, src_vals + s0, cnt * sizeof(double),
                            cudaMemcpyHostToDevice, h->stream));
         h->launches_last = 0;
+        const int p0 = h->parity;
         int rc = set_run_buffers(h, n0 + s0, h->d_src, h->d_probe, h->d_iters);
         if (!rc) rc = enqueue_steps(h, cnt);
         if (rc) return rc;
+        mpb_failure fl;
+        rc = read_failure(h, &fl);
+        // a multi-rank step whose global residual went back above tol was
+        // suspended (every later step of the chunk did nothing): continue it
+        // on the host, then run the rest of the chunk
+        while (rc == MPB_ESTEP && fl.kind == kMpbSuspend) {
+            const int64_t k = fl.step - (n0 + s0);     // index within the chunk
+            h->parity = p0 ^ (int)(k & 1);
+            if ((rc = recover_suspended(&h, 1, false, h->stream))) return rc;
+            h->parity ^= 1;
+            rc = read_failure(h, &fl);
+            if (rc != MPB_OK) break;                   // the continuation failed
+            if ((rc = enqueue_steps(h, cnt - k - 1))) return rc;
+            rc = read_failure(h, &fl);
+        }
         launches += h->launches_last;
         if (h->nprobes && probe_out)
             CU(cudaMemcpyAsync(probe_out + s0 * h->nprobes, h->d_probe,
@@ -1180,8 +1296,7 @@ int mpb_run(mpb_handle* h, int64_t n0, int64_t nsteps, const double* src_vals,
         if (iters_out)
             CU(cudaMemcpyAsync(iters_out + s0, h->d_iters, cnt * sizeof(int),
                                cudaMemcpyDeviceToHost, h->stream));
-        mpb_failure fl;
-        rc = read_failure(h, &fl);
+        CU(cudaStreamSynchronize(h->stream));
         if (rc == MPB_ESTEP) {
             if (fail) *fail = fl;
             h->launches_last = launches;
@@ -1287,11 +1402,26 @@ int mpb_group_run(mpb_handle* const* hs, int32_t n, int64_t n0, int64_t nsteps,
         CU(cudaMalloc(&dprobe[(size_t)r], cnt * std::max(1, hs[r]->nprobes) * sizeof(double)));
         rc = set_run_buffers(hs[r], n0, dsrc, dprobe[(size_t)r], diters + r * cnt);
     }
-    for (int64_t t = 0; t < nsteps && !rc; ++t) {
-        rc = group_step(hs, n, hs[0]->parity, s);
+    int64_t t = 0;
+    while (t < nsteps && !rc) {
+        const int64_t t0 = t;
+        const int p0 = hs[0]->parity;
+        for (; t < nsteps && !rc; ++t) {
+            rc = group_step(hs, n, hs[0]->parity, s);
+            for (int r = 0; r < n; ++r) hs[r]->parity ^= 1;
+        }
+        if (!rc) rc = drain_exchange(hs[0], s);
+        if (rc) break;
+        mpb_failure fl;
+        if (read_failure(hs[0], &fl) != MPB_ESTEP || fl.kind != kMpbSuspend) break;
+        // suspended step (see recover_suspended): continue it, then go on
+        const int64_t k = fl.step - n0;
+        for (int r = 0; r < n; ++r) hs[r]->parity = p0 ^ (int)((k - t0) & 1);
+        rc = recover_suspended(hs, n, true, s);
         for (int r = 0; r < n; ++r) hs[r]->parity ^= 1;
+        t = k + 1;
+        if (!rc && read_failure(hs[0], &fl) == MPB_ESTEP) break;
     }
-    if (!rc) rc = drain_exchange(hs[0], s);
     if (!rc) {
         CU(cudaStreamSynchronize(s));
         for (int r = 0; r < n; ++r)
@@ -1374,6 +1504,8 @@ int mpb_comm_info(mpb_handle* h, int32_t* nranks, int32_t* rank, int32_t* nccl_v
 }
 
 int64_t mpb_launch_count(mpb_handle* h) { return h ? h->launches_last : 0; }
+
+int64_t mpb_continued_steps(mpb_handle* h) { return h ? h->continued_steps : 0; }
 
 int mpb_sweep_form(mpb_handle* h, int32_t out[4]) {
     g_err.clear();

@@ -306,10 +306,15 @@ __global__ void __launch_bounds__(256) k_llg_fixup(Geom g, Bufs b,
 //    iterates 1..R' are all-reduced into hist2, and k_llg_decide replays the
 //    rule on hist2.  A cell that had stopped earlier cannot make hist2[r]
 //    <= tol for r < R' (the cell with r_c = R' is still > tol there), so the
-//    rule stops at R' unless the global residual is non-monotone at R'
-//    (a cell back above tol) -- then the step is flagged (kind 3) instead of
-//    silently diverging from the reference.
+//    rule stops at R' -- unless the global residual is non-monotone at R'
+//    (a cell that stopped early is back above tol).  The reference then
+//    keeps iterating (llg.py:131-148); the step is suspended (kMpbSuspend:
+//    every later kernel of the chunk is a no-op) and the host continues it
+//    in lockstep, one iterate and one all-reduce at a time
+//    (k_llg_cont_*, mpb_api.cu recover_suspended), then resumes the run.
 // ---------------------------------------------------------------------------
+constexpr int kMpbSuspend = 4;   // StepState.fail_kind of a suspended step
+
 __global__ void __launch_bounds__(256) k_llg_topup(Geom g, Bufs b,
                                                    const mpb_material* __restrict__ mats,
                                                    const uint8_t* __restrict__ ids,
@@ -391,8 +396,11 @@ __global__ void k_llg_decide(Geom g, StepState* st) {
         const int R = min(rmax, g.max_iters);
         r = llg_decide(st->hist2, R, g.max_iters, g.tol, &fr, &fi, &fk);
         st->fixup_ran = 1;
-        if (r > 0 && r != R) { r = -1; }
-        if (r < 0) { fr = bitsd(st->hist2[R]); fi = R; fk = 3; r = 0; }
+        if (r < 0) {   // still above tol at R: continue on the host (see above)
+            st->fail = 1; st->fail_step = st->step; st->fail_res = bitsd(st->hist2[R]);
+            st->fail_it = R; st->fail_kind = kMpbSuspend;
+            return;
+        }
     }
     if (r > 0) {
         st->rstar = r;
@@ -400,6 +408,96 @@ __global__ void k_llg_decide(Geom g, StepState* st) {
         st->fail = 1; st->fail_step = st->step; st->fail_res = fr;
         st->fail_it = fi; st->fail_kind = fk;
     }
+}
+
+// Lockstep continuation of a suspended multi-rank step (host-driven, one
+// iterate per launch).  Scratch per local cell: Hn[3] Mn[3] cE[3] Mr[3].
+__global__ void __launch_bounds__(256) k_llg_cont_init(Geom g, Bufs b,
+                                                       const int2* __restrict__ cells, int n,
+                                                       MagScratch scr) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= n) return;
+    const int i = cells[q].x, f = cells[q].y;
+    const int64_t o = i * g.PP + f;
+    const int64_t om = (int64_t)(i - g.mx0) * g.PP + f;
+    const Curl3 c = curl_e_at(g, b.Ea, o, g.PP, g.F[2], true, true, true);
+    double* w = scr.v + (size_t)q * 12;
+    for (int k = 0; k < 3; ++k) {
+        w[k] = b.Ha[k][o];
+        w[3 + k] = b.Ma[k][om];
+        w[9 + k] = w[3 + k];
+    }
+    w[6] = c.x; w[7] = c.y; w[8] = c.z;
+}
+
+// iterate r of every local cell (llg.py:131-137); owned cells' residuals
+// max-reduced into st->hist2[r]
+__global__ void __launch_bounds__(256) k_llg_cont_iter(Geom g,
+                                                       const mpb_material* __restrict__ mats,
+                                                       const uint8_t* __restrict__ ids,
+                                                       const int2* __restrict__ cells,
+                                                       const unsigned char* __restrict__ owned,
+                                                       int n, MagScratch scr, StepState* st,
+                                                       int r) {
+    __shared__ unsigned long long red[8];
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long lmax = 0ull;
+    if (q < n) {
+        const int i = cells[q].x, f = cells[q].y;
+        double* w = scr.v + (size_t)q * 12;
+        LlgCell s;
+        for (int c = 0; c < 3; ++c) { s.Hn[c] = w[c]; s.Mn[c] = w[3 + c]; s.cE[c] = w[6 + c]; }
+        llg_setup(s, mats[ids[i * g.PP + f]]);
+        double Mr[3] = {w[9], w[10], w[11]};
+        double Hr[3];
+        for (int c = 0; c < 3; ++c)   // H^{n+1,r-1} (llg.py:105); H^n before iterate 1
+            Hr[c] = r == 1 ? s.Hn[c] : (s.Hn[c] + (s.Mn[c] - Mr[c])) - g.coef_h * s.cE[c];
+        const unsigned long long rb = dbits(llg_iterate(s, g.coef_h, Hr, Mr));
+        if (owned[q]) lmax = rb;
+        w[9] = Mr[0]; w[10] = Mr[1]; w[11] = Mr[2];
+    }
+    for (int sh = 16; sh > 0; sh >>= 1) {
+        const unsigned long long o2 = __shfl_xor_sync(0xffffffffu, lmax, sh);
+        lmax = o2 > lmax ? o2 : lmax;
+    }
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = lmax;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long x = 0ull;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) x = red[w] > x ? red[w] : x;
+        if (x) atomicMax(&st->hist2[r], x);
+    }
+}
+
+// the settled iterate r*: H^{n+1} (every local cell) and M^{n+1} (owned)
+__global__ void __launch_bounds__(256) k_llg_cont_write(Geom g, Bufs b,
+                                                        const int2* __restrict__ cells,
+                                                        const unsigned char* __restrict__ owned,
+                                                        int n, MagScratch scr, StepState* st,
+                                                        int rstar) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q == 0) { st->rstar = rstar; st->fixup_ran = 1; }
+    if (q >= n) return;
+    const int i = cells[q].x, f = cells[q].y;
+    const int64_t o = i * g.PP + f;
+    const int64_t om = (int64_t)(i - g.mx0) * g.PP + f;
+    const double* w = scr.v + (size_t)q * 12;
+    for (int c = 0; c < 3; ++c) {
+        b.Hb[c][o] = (w[c] + (w[3 + c] - w[9 + c])) - g.coef_h * w[6 + c];
+        if (owned[q]) b.Mb[c][om] = w[9 + c];
+    }
+}
+
+// Clear a suspension (and the lockstep history) before the host continues
+// the step; record a failure the host-driven continuation found.
+__global__ void k_suspend_clear(StepState* st, int max_iters) {
+    for (int r = threadIdx.x; r <= max_iters + 1; r += blockDim.x) st->hist2[r] = 0ull;
+    if (threadIdx.x == 0) { st->fail = 0; st->fail_kind = 0; st->fail_step = -1; }
+}
+
+__global__ void k_set_failure(StepState* st, double res, int it, int kind) {
+    st->fail = 1; st->fail_step = st->step; st->fail_res = res;
+    st->fail_it = it; st->fail_kind = kind;
 }
 
 // ---------------------------------------------------------------------------

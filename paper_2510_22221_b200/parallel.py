@@ -145,7 +145,8 @@ def slab_device_runs(config, materials, keys, slabs, device=0, **kw):
     return runs
 
 
-def run_group(config, nranks: int, bias=None, device: int = 0, state=None, start: int = 0):
+def run_group(config, nranks: int, bias=None, device: int = 0, state=None, start: int = 0,
+              stats: dict | None = None):
     """Run ``config`` as an ``nranks``-slab decomposition emulated on one GPU
     (mpb_group_run).  Returns (fields dict, M, probes dict, iterations) in
     the global layout -- must equal sim.run bit for bit.  ``state`` (global
@@ -186,6 +187,8 @@ def run_group(config, nranks: int, bias=None, device: int = 0, state=None, start
             return None, None, None, (int(fail.step), float(fail.residual),
                                       int(fail.iterations), int(fail.kind))
         N.check(code)
+        if stats is not None:
+            stats["continued_steps"] = int(N.load_library().mpb_continued_steps(runs[0].h))
         fields = {n: np.empty(fs) for n in ("Ex", "Ey", "Ez", "Hx", "Hy", "Hz")}
         M = np.empty((3,) + config.grid.cell_shape)
         for r, sl in zip(runs, slabs):

@@ -174,9 +174,9 @@ def _raise_failure(fail, config):
     if kind == 1:
         msg = (f"fixed-point iteration diverging (residual {res:.3e} "
                f"after {it} iterates)")
-    elif kind == 3:
-        msg = (f"fixed-point iteration: global residual non-monotone across ranks "
-               f"at iterate {it} (residual {res:.3e})")
+    elif kind == 4:   # only from mpb_run_device (mpb_run continues the step)
+        msg = (f"multi-rank step suspended: global residual back above tol at "
+               f"iterate {it} (residual {res:.3e}); continue it through mpb_run")
     else:
         msg = (f"fixed-point iteration did not reach tol "
                f"{config.llg_params.tol:.1e} in "

@@ -61,6 +61,24 @@ CASES = {
         probes=[("Ey", 5, 8, 8), ("Hx", 8, 8, 8), ("Mx", 8, 8, 8),
                 ("My", 8, 8, 8), ("Mz", 8, 8, 8)],
     ),
+    # pec_block with a tolerance at which the global residual is
+    # NON-MONOTONE in some steps (6 and 14): a cell whose own residual fell
+    # below tol at iterate 1 is back above it at iterate 2, so the reference
+    # keeps iterating past the last local stop (llg.py:131-148) -- the case
+    # the multi-rank continuation (recover_suspended) exists for
+    "nonmono3d": dict(
+        grid=(16, 16, 16, 10e-6, 10e-6, 10e-6),
+        background=(0.0, 1.0),
+        boxes=[dict(box=(6, 10, 6, 10, 6, 10), eps_r=15.0, Ms=1.3926e5,
+                    alpha=1e-3, bias=1000.0 * OE, bias_direction=(0, 0, 1))],
+        source=dict(f0=50e9, Tp=1e-12, amplitude=1e8, location=(4, 8, 8),
+                    polarization=(0.0, 1.0, 0.0)),
+        boundaries=dict(x0="PEC", x1="PEC", y0="PEC", y1="PEC", z0="PEC",
+                        z1="PEC"),
+        cfl=0.9, steps=150, llg=(5.5e-8, 50),
+        probes=[("Ey", 5, 8, 8), ("Hx", 8, 8, 8), ("Mx", 8, 8, 8),
+                ("My", 8, 8, 8), ("Mz", 8, 8, 8)],
+    ),
     # 2D (collapsed z): PMC/MUR/PEC in-plane faces
     "plane2d": dict(
         grid=(14, 12, 1, 4e-6, 6e-6, 3e-6),
@@ -113,6 +131,7 @@ CASES = {
     ),
     # fault injection: tolerance no iterate can meet in one step
     "fail_tol": dict(
+        expect_failure=True,
         grid=(1, 1, 120, 2e-6, 2e-6, 2e-6),
         background=(1e-4, 8.0),
         boxes=[dict(box=(0, 1, 0, 1, 60, 61), sigma=1e-3, eps_r=1.0, Ms=9.7e5,
@@ -212,6 +231,7 @@ CASES = {
     # StepFailure in 3D: many magnetic cells, a budget of 2 iterates and a
     # tolerance no step can meet (the failure comes from the global rule)
     "fail3d": dict(
+        expect_failure=True,
         grid=(9, 8, 7, 6e-6, 6e-6, 5e-6),
         background=(0.0, 1.5),
         boxes=[dict(box=(2, 7, 2, 6, 2, 5), eps_r=15.0, Ms=1.3926e5, alpha=1e-3,

@@ -39,7 +39,10 @@ def main() -> None:
     from magphon import sim as rsim
 
     rns, mns = reference_namespace(), mirror_namespace()
+    only = sys.argv[1:]           # optional case names: regenerate just those
     for name, case in CASES.items():
+        if only and name not in only:
+            continue
         rcfg = build(case, rns)
         mcfg = build(case, mns)
         bias = case.get("bias")
@@ -73,12 +76,19 @@ def main() -> None:
                 payload[_probe_key(key)] = ser.samples
             mixed = sum(int(len(set(f.tolist())) > 1) for f in mine["first_converged"])
             payload["mixed_steps"] = np.int64(mixed)
+            # steps whose r* exceeds every cell's own first stop: the global
+            # residual went back above tol after the last local stop
+            nonmono = sum(int(f.size and int(f.max()) < int(r))
+                          for f, r in zip(mine["first_converged"], ref.iterations))
+            payload["nonmono_steps"] = np.int64(nonmono)
             its = ref.iterations
             print(f"{name}: {ref.steps} steps, r* histogram "
                   f"{dict(zip(*np.unique(its, return_counts=True))) if its.size else {}}, "
-                  f"steps with per-cell stop disagreement: {mixed}")
+                  f"steps with per-cell stop disagreement: {mixed}, non-monotone: {nonmono}")
         np.savez_compressed(OUT / f"{name}.npz", **payload)
 
+    if only:
+        return
     # snapshot / resume golden on mixed3d (sim.py:187-220)
     rcfg = build(CASES["mixed3d"], rns)
     snap = rsim.snapshot_state(rcfg, None, 47)

@@ -16,7 +16,7 @@ from tests.golden_io import load
 pytestmark = pytest.mark.gpu
 
 VARIANTS = [0, 1]
-RUNNING = [n for n in CASES if "llg" not in CASES[n]]
+RUNNING = [n for n in CASES if not CASES[n].get("expect_failure")]
 
 
 def _assert_same(res, g):

@@ -15,7 +15,10 @@ pytestmark = pytest.mark.gpu
 SPLITS = [("mixed3d", 2), ("mixed3d", 3), ("allmur3d", 2), ("allmur3d", 5),
           ("pec_block", 4), ("zwall_magnet", 2), ("zwall_magnet", 3), ("thin", 3),
           ("plane2d", 2), ("xline1d", 4), ("bias3d", 2), ("plane_xz", 3),
-          ("cpw_small", 3), ("two_magnets", 2), ("two_magnets", 4)]
+          ("cpw_small", 3), ("two_magnets", 2), ("two_magnets", 4),
+          # global residual non-monotone past the last local stop: the
+          # suspended step is continued in lockstep on the host
+          ("nonmono3d", 2), ("nonmono3d", 3)]
 
 
 @pytest.mark.parametrize("name,nranks", SPLITS)
@@ -39,7 +42,7 @@ def test_slab_group_matches_reference_golden(name, nranks):
 # chunks (after them); MPB_OVERLAP=0 is the serialised order.
 @pytest.mark.parametrize("overlap", ["1", "0"])
 @pytest.mark.parametrize("name,nranks", [("mixed3d", 2), ("pec_block", 2), ("bias3d", 2),
-                                         ("allmur3d", 2)])
+                                         ("allmur3d", 2), ("nonmono3d", 2)])
 def test_slab_overlapped_exchange_matches_golden(name, nranks, overlap, monkeypatch):
     monkeypatch.setenv("MPB_SWEEP_MINCHUNK", "2")
     monkeypatch.setenv("MPB_OVERLAP", overlap)
@@ -93,3 +96,18 @@ def test_slab_group_step_failure(nranks):
     assert step == int(g["fail_step"])
     assert residual == float(g["fail_residual"])
     assert iterations == int(g["fail_iterations"])
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_slab_group_continues_nonmonotone_steps(nranks):
+    """nonmono3d's steps 6 and 14 have a global residual back above tol after
+    every cell's own stop: the reference iterates on (llg.py:131-148), and
+    the slab path must suspend and continue exactly those steps."""
+    g = load("nonmono3d")
+    cfg = build(CASES["nonmono3d"], mirror_namespace())
+    stats = {}
+    fields, M, probes, its = parallel.run_group(cfg, nranks, stats=stats)
+    assert fields is not None, its
+    assert stats["continued_steps"] == int(g["nonmono_steps"]) == 2
+    assert np.array_equal(its, g["iterations"])
+    assert np.array_equal(M, g["fields"]["M"])
