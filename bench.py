@@ -58,15 +58,18 @@ def _peaks():
     return FALLBACK_HBM, "fallback"
 
 
-def _bytes_per_cell(f_mag: float) -> float:
-    # 6 field comps read+written once (96 B fp64) + M read+write
-    # (48 B) in the magnetic fraction.  Ids/halos/probes are not credited.
-    return 96.0 + 48.0 * f_mag
+def _bytes_per_cell(f_mag: float, dtype: str = "f64") -> float:
+    # 6 field comps read+written once (96 B fp64, 48 B fp32) + M
+    # read+write (48 B; M is fp64 in both storage modes) in the magnetic
+    # fraction.  Ids/halos/probes are not credited.
+    return _sweep_bytes(dtype) + 48.0 * f_mag
 
 
-# The dominant kernel (k_sweep) moves the six field components; M is read and
-# written by k_llg_local, so the sweep's algorithmic bytes are 96 B/cell.
-SWEEP_BYTES_PER_CELL = 96.0
+def _sweep_bytes(dtype: str) -> float:
+    # The dominant kernel (k_sweep) moves the six field components; M is read
+    # and written by k_llg_local, so the sweep's algorithmic bytes are 96
+    # B/cell (48 B/cell in the fp32 storage mode).
+    return 96.0 if dtype == "f64" else 48.0
 
 
 class ClockSampler:
@@ -194,8 +197,9 @@ def slab_run(cfg, keys, world, rank, local, args, nccl: bool = True):
             else cfg.materials.region(c0, c1))
     a = _device_run_args(gcfg, keys)
     dev = _device_class()(ggrid, mats, a["boundaries"], a["source_loc"], a["source_pol"], keys,
-                    cfg.llg_params, cfg.dt, device=local, kernel_variant=args.variant,
-                    slab=slab)
+                          cfg.llg_params, cfg.dt, device=local, kernel_variant=args.variant,
+                          slab=slab, **({"storage": args.dtype}
+                                        if getattr(args, "dtype", "f64") != "f64" else {}))
     f0, f1 = slab.field_range
     st = synthetic_state((f1 - f0,) + tuple(ggrid.field_shape[1:]), args.init)
     dev.load_state(st, initial_magnetization(mats))
@@ -349,12 +353,14 @@ def workload_config(args, cfg, world: int, total_cells: int) -> dict:
     return {"workload": f"{args.config.upper()} {'x'.join(map(str, g.cell_shape))} "
                         + ("cells per GPU" if args.scaling == "weak" else
                            f"cells split over {world} GPU(s)")
-                        + f", {DESCRIPTIONS[args.config]}, fp64",
+                        + f", {DESCRIPTIONS[args.config]}, "
+                        + ("fp64" if getattr(args, "dtype", "f64") == "f64"
+                           else "fp32 E/H storage (M + LLG fp64)"),
             "config_file": CONFIGS[args.config], "cells_per_gpu": per_gpu,
             "cells_total": total_cells,
             "magnetic_fraction": cfg.materials.magnetic_count() / cells,
             "parallelism": f"x-slab x{world}" if world > 1 else "single GPU",
-            "l2": "state (2 x 6 fp64 fields) >> 126 MB L2; no flush needed",
+            "l2": "state (2 x 6 field arrays) >> 126 MB L2; no flush needed",
             "kernel_variant": args.variant,
             "initial_state": args.init}
 
@@ -404,6 +410,9 @@ def main() -> None:
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--variant", type=int, default=0)
+    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"],
+                    help="field storage: f64 (reference precision, bit-exact; the "
+                         "headline) or f32 (opt-in, E/H in fp32, M + LLG in fp64)")
     ap.add_argument("--cpu-planes", type=int, default=32,
                     help="x-planes of the bench config in the 1-core cpu_baseline sample")
     ap.add_argument("--cpu-steps", type=int, default=8)
@@ -452,7 +461,7 @@ def main() -> None:
     keys = list(dict.fromkeys(keys))
     if world == 1:
         dev = sim._device_run(cfg, cfg.materials, keys, device=local,
-                              kernel_variant=args.variant)
+                              kernel_variant=args.variant, storage=args.dtype)
         dev.load_state(synthetic_state(cfg.grid.field_shape, args.init),
                        initial_magnetization(cfg.materials))
         rank_cells = cells
@@ -536,14 +545,15 @@ def main() -> None:
         t_e2e = float(t.item())
     e2e = total_cells * e2e_steps / t_e2e / 1e9
     peak, peak_kind = _peaks()
-    bpc = SWEEP_BYTES_PER_CELL if kname == "k_sweep" else _bytes_per_cell(f_mag)
+    bpc = _sweep_bytes(args.dtype) if kname == "k_sweep" else _bytes_per_cell(f_mag, args.dtype)
     per_launch_ms = kms / max(1, klaunch)
     achieved = rank_cells * bpc / (per_launch_ms * 1e-3) / 1e9 if klaunch else None
-    step_frac = value / world * _bytes_per_cell(f_mag) / peak   # per-GPU average
+    step_frac = value / world * _bytes_per_cell(f_mag, args.dtype) / peak   # per-GPU average
     traffic = None
     tp = ROOT / "profiles" / "traffic.json"
     if tp.exists() and args.config == "c4" and world == 1:   # captured on C4, 1 GPU
-        traffic = json.loads(tp.read_text()).get(kname)
+        traffic = json.loads(tp.read_text()).get(kname if args.dtype == "f64"
+                                                 else f"{kname}_{args.dtype}")
     comm = dev.comm_info()
     if world > 1:
         gathered = [None] * world
@@ -566,7 +576,7 @@ def main() -> None:
         "metric": METRIC, "value": value, "unit": "Gcell-updates/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms / args.steps, "higher_is_better": True,
-        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": args.dtype,
         "data": "synthetic",
         "config": workload_config(args, cfg, world, total_cells),
         "e2e": {"value": e2e, "unit": "Gcell-updates/s",
@@ -579,7 +589,7 @@ def main() -> None:
                      "kernel_ms_per_step": per_launch_ms,
                      "kernel_share_of_step": per_launch_ms / (ms / args.steps),
                      "whole_step_frac": step_frac,
-                     "whole_step_bytes_per_cell": _bytes_per_cell(f_mag)},
+                     "whole_step_bytes_per_cell": _bytes_per_cell(f_mag, args.dtype)},
         "cpu_baseline": cpu,
         "clocks": clk.summary(t_wall0, t_wall1),
         "gpu_launches": launches,

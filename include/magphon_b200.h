@@ -20,7 +20,9 @@
  *  - A handle owns all of its device memory and streams; it is not
  *    thread-safe.  Do not fork after mpb_create.
  *  - Arithmetic is IEEE fp64 without FMA contraction, in the reference's
- *    operation order, so results are bit-identical to the reference CPU path.
+ *    operation order, so results are bit-identical to the reference CPU path
+ *    (the opt-in fp32 field storage, mpb_setup.storage, trades that for half
+ *    the HBM traffic and is held to a tolerance instead).
  */
 #ifndef MAGPHON_B200_H
 #define MAGPHON_B200_H
@@ -105,7 +107,16 @@ typedef struct mpb_setup {
     int32_t x_lo, x_hi;
     int32_t any_magnetic;   /* 1 if any rank owns magnetic cells             */
     uint8_t nccl_id[128];   /* ncclUniqueId from mpb_nccl_unique_id (rank 0) */
+    /* Field storage: MPB_STORAGE_F64 (default; the reference's fp64, results
+     * bit-identical) or MPB_STORAGE_F32 (opt-in: E and H stored and updated
+     * in fp32 -- 48 B/cell instead of 96 -- while M and the whole LLG fixed
+     * point stay fp64; agrees with the fp64 reference within a stated
+     * tolerance, not bitwise.  Fused sweep only, no line kernel). */
+    int32_t storage;
 } mpb_setup;
+
+#define MPB_STORAGE_F64 0
+#define MPB_STORAGE_F32 1
 
 /* Failure record of an LLG step (llg.py:139-148 + sim.py:161-164). */
 typedef struct mpb_failure {

@@ -45,7 +45,11 @@ class Setup(C.Structure):
                 ("graph_steps", C.c_int32),
                 ("nranks", C.c_int32), ("rank", C.c_int32),
                 ("x_lo", C.c_int32), ("x_hi", C.c_int32),
-                ("any_magnetic", C.c_int32), ("nccl_id", C.c_uint8 * 128)]
+                ("any_magnetic", C.c_int32), ("nccl_id", C.c_uint8 * 128),
+                ("storage", C.c_int32)]
+
+
+STORAGE_CODES = {"f64": 0, "f32": 1}
 
 
 class Failure(C.Structure):

@@ -80,8 +80,10 @@ struct mpb_handle {
                                    // share one concurrently
     int64_t nloc = 0;              // (hi - lo) * PP
     int64_t mplanes = 0;           // mx1 - mx0
-    double* E[2][3] = {};          // allocations (local planes)
-    double* H[2][3] = {};
+    void* E[2][3] = {};            // allocations (local planes); element type
+    void* H[2][3] = {};            // double, or float in the fp32 storage mode
+    int f32 = 0;                   // fp32 storage of E/H (M stays fp64)
+    size_t esz = sizeof(double);   // bytes per E/H element
     double* M[2][3] = {};
     uint8_t* ids = nullptr;        // allocation (local planes)
     mpb_material* mats = nullptr;
@@ -143,12 +145,16 @@ namespace {
 // Fused single-sweep variant hooks (mpb_fused.cuh).
 int prepare_fused(mpb_handle* h, const Geom& g);
 void destroy_fused(mpb_handle* h);
-int launch_fused(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s, int part,
+template <typename T>
+int launch_fused(mpb_handle* h, const Geom& g, const BufsT<T>& b, cudaStream_t s, int part,
                  int64_t& launches);
-int launch_deferred(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s);
-int launch_zfix(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s);
+template <typename T>
+int launch_deferred(mpb_handle* h, const Geom& g, const BufsT<T>& b, cudaStream_t s);
+template <typename T>
+int launch_zfix(mpb_handle* h, const Geom& g, const BufsT<T>& b, cudaStream_t s);
 int zfix_launches(mpb_handle* h);
-int launch_llg_local(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s);
+template <typename T>
+int launch_llg_local(mpb_handle* h, const Geom& g, const BufsT<T>& b, cudaStream_t s);
 const char* fused_kernel_name();
 void fused_form(mpb_handle* h, int32_t out[4]);
 }  // namespace
@@ -162,15 +168,22 @@ T* view(T* alloc, const mpb_handle* h) {
     return alloc ? alloc - (int64_t)h->lo * h->g.PP : nullptr;
 }
 
-Bufs make_bufs(const mpb_handle* h, int pa) {
-    Bufs b{};
+// typed view of an E/H allocation (storage type T)
+template <typename T>
+T* fview(void* alloc, const mpb_handle* h) {
+    return view(static_cast<T*>(alloc), h);
+}
+
+template <typename T>
+BufsT<T> make_bufs(const mpb_handle* h, int pa) {
+    BufsT<T> b{};
     const int pb = 1 - pa;
     for (int c = 0; c < 3; ++c) {
-        b.Ea[c] = view(h->E[pa][c], h);
-        b.Ha[c] = view(h->H[pa][c], h);
+        b.Ea[c] = fview<T>(h->E[pa][c], h);
+        b.Ha[c] = fview<T>(h->H[pa][c], h);
         b.Ma[c] = h->M[pa][c];      // M arrays are indexed (i - mx0) already
-        b.Eb[c] = view(h->E[pb][c], h);
-        b.Hb[c] = view(h->H[pb][c], h);
+        b.Eb[c] = fview<T>(h->E[pb][c], h);
+        b.Hb[c] = fview<T>(h->H[pb][c], h);
         b.Mb[c] = h->M[pb][c];
     }
     return b;
@@ -220,6 +233,20 @@ int dev_alloc(mpb_handle* h, T** p, size_t count) {
     return MPB_OK;
 }
 
+// E/H field allocation of `count` elements of the handle's storage type
+int field_alloc(mpb_handle* h, void** p, size_t count) {
+    if (h->f32) {
+        float* q = nullptr;
+        const int rc = dev_alloc(h, &q, count);
+        *p = q;
+        return rc;
+    }
+    double* q = nullptr;
+    const int rc = dev_alloc(h, &q, count);
+    *p = q;
+    return rc;
+}
+
 void dev_free(mpb_handle* h, void* p) {
     if (!p) return;
     if (guard_mode()) {
@@ -264,7 +291,10 @@ int reset_state(mpb_handle* h) {
 int exchange(mpb_handle* h, int pb, cudaStream_t s) {
     const Geom& g = h->g;
     const size_t n = (size_t)g.PP;
-    auto plane = [&](double* alloc, int i) { return alloc + (int64_t)(i - h->lo) * g.PP; };
+    const ncclDataType_t ft = h->f32 ? ncclFloat : ncclDouble;   // E/H element type
+    auto plane = [&](void* alloc, int i) {
+        return static_cast<char*>(alloc) + (int64_t)(i - h->lo) * g.PP * (int64_t)h->esz;
+    };
     auto mplane = [&](double* alloc, int i) { return alloc + (int64_t)(i - g.mx0) * g.PP; };
     auto has_m = [&](int i) { return h->mplanes > 0 && i >= g.mx0 && i < g.mx1; };
     ncclComm_t xc = h->comm_x ? h->comm_x : h->comm;
@@ -272,21 +302,23 @@ int exchange(mpb_handle* h, int pb, cudaStream_t s) {
     if (h->rank + 1 < h->nranks) {
         const int up = h->rank + 1;
         for (int c = 0; c < 3; ++c) {
-            NC(ncclSend(plane(h->E[pb][c], g.c1 - 1), n, ncclDouble, up, xc, s));
-            NC(ncclSend(plane(h->H[pb][c], g.c1 - 1), n, ncclDouble, up, xc, s));
+            NC(ncclSend(plane(h->E[pb][c], g.c1 - 1), n, ft, up, xc, s));
+            NC(ncclSend(plane(h->H[pb][c], g.c1 - 1), n, ft, up, xc, s));
             if (has_m(g.c1 - 1))
                 NC(ncclSend(mplane(h->M[pb][c], g.c1 - 1), n, ncclDouble, up, xc, s));
-            NC(ncclRecv(plane(h->E[pb][c], g.c1), n, ncclDouble, up, xc, s));
+            // the high ghost plane feeds only dEz/dx, dEy/dx of plane c1-1:
+            // its Ex is never read, so it does not travel
+            if (c > 0) NC(ncclRecv(plane(h->E[pb][c], g.c1), n, ft, up, xc, s));
         }
     }
     if (h->rank > 0) {
         const int dn = h->rank - 1;
         for (int c = 0; c < 3; ++c) {
-            NC(ncclRecv(plane(h->E[pb][c], g.c0 - 1), n, ncclDouble, dn, xc, s));
-            NC(ncclRecv(plane(h->H[pb][c], g.c0 - 1), n, ncclDouble, dn, xc, s));
+            NC(ncclRecv(plane(h->E[pb][c], g.c0 - 1), n, ft, dn, xc, s));
+            NC(ncclRecv(plane(h->H[pb][c], g.c0 - 1), n, ft, dn, xc, s));
             if (has_m(g.c0 - 1))
                 NC(ncclRecv(mplane(h->M[pb][c], g.c0 - 1), n, ncclDouble, dn, xc, s));
-            NC(ncclSend(plane(h->E[pb][c], g.c0), n, ncclDouble, dn, xc, s));
+            if (c > 0) NC(ncclSend(plane(h->E[pb][c], g.c0), n, ft, dn, xc, s));
         }
     }
     NC(ncclGroupEnd());
@@ -297,15 +329,18 @@ int exchange(mpb_handle* h, int pb, cudaStream_t s) {
 
 // part 0: whole sweep + LLG; 1: interior chunks only (overlaps the slab
 // exchange of the previous step); 2: edge chunks + LLG (after the exchange).
-int phase_sweep(mpb_handle* h, int pa, cudaStream_t s, int64_t& launches, int part = 0) {
+template <typename T>
+int phase_sweep_t(mpb_handle* h, int pa, cudaStream_t s, int64_t& launches, int part) {
     const Geom& g = h->g;
-    const Bufs b = make_bufs(h, pa);
-    const size_t hist_smem = (size_t)(g.max_iters + 2) * sizeof(unsigned long long);
-    const dim3 plane_grid((g.FyFz + 255) / 256, g.c1 - g.c0);
-    if (h->variant == 1) {
-        k_hsweep<<<plane_grid, 256, hist_smem, s>>>(g, b, h->mats, ids_view(h), h->st);
-        ++launches;
-        return MPB_OK;
+    const BufsT<T> b = make_bufs<T>(h, pa);
+    if constexpr (sizeof(T) == 8) {
+        if (h->variant == 1) {
+            const size_t hist_smem = (size_t)(g.max_iters + 2) * sizeof(unsigned long long);
+            const dim3 plane_grid((g.FyFz + 255) / 256, g.c1 - g.c0);
+            k_hsweep<<<plane_grid, 256, hist_smem, s>>>(g, b, h->mats, ids_view(h), h->st);
+            ++launches;
+            return MPB_OK;
+        }
     }
     int rc = launch_fused(h, g, b, s, part, launches);
     if (rc) return rc;
@@ -314,6 +349,11 @@ int phase_sweep(mpb_handle* h, int pa, cudaStream_t s, int64_t& launches, int pa
         ++launches;
     }
     return MPB_OK;
+}
+
+int phase_sweep(mpb_handle* h, int pa, cudaStream_t s, int64_t& launches, int part = 0) {
+    return h->f32 ? phase_sweep_t<float>(h, pa, s, launches, part)
+                  : phase_sweep_t<double>(h, pa, s, launches, part);
 }
 
 // Sweep of a slab step: when the previous step's boundary exchange is still
@@ -337,10 +377,11 @@ int phase_sweep_overlapped(mpb_handle* const* hs, int n, int pa, cudaStream_t s,
     return MPB_OK;
 }
 
-int phase_fixup_single(mpb_handle* h, int pa, cudaStream_t s, int64_t& launches) {
+template <typename T>
+int phase_fixup_single_t(mpb_handle* h, int pa, cudaStream_t s, int64_t& launches) {
     if (h->nmag == 0) return MPB_OK;
     const Geom& g = h->g;
-    const Bufs b = make_bufs(h, pa);
+    const BufsT<T> b = make_bufs<T>(h, pa);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(h->fixup_blocks);
     cfg.blockDim = dim3(256);
@@ -354,20 +395,31 @@ int phase_fixup_single(mpb_handle* h, int pa, cudaStream_t s, int64_t& launches)
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     MagScratch scr{h->scratch};
-    CU(cudaLaunchKernelEx(&cfg, k_llg_fixup, g, b, (const mpb_material*)h->mats, ids_view(h),
-                          (const int2*)h->magcells, h->nmag, scr, h->st));
+    CU(cudaLaunchKernelEx(&cfg, k_llg_fixup<T>, g, b, (const mpb_material*)h->mats,
+                          ids_view(h), (const int2*)h->magcells, h->nmag, scr, h->st));
+    ++launches;
+    return MPB_OK;
+}
+
+int phase_fixup_single(mpb_handle* h, int pa, cudaStream_t s, int64_t& launches) {
+    return h->f32 ? phase_fixup_single_t<float>(h, pa, s, launches)
+                  : phase_fixup_single_t<double>(h, pa, s, launches);
+}
+
+template <typename T>
+int phase_topup_t(mpb_handle* h, int pa, cudaStream_t s, int64_t& launches) {
+    if (h->nmag == 0) return MPB_OK;
+    const BufsT<T> b = make_bufs<T>(h, pa);
+    k_llg_topup<T><<<(h->nmag + 255) / 256, 256, 0, s>>>(h->g, b, h->mats, ids_view(h),
+                                                         h->magcells, h->magowned, h->nmag,
+                                                         h->st);
     ++launches;
     return MPB_OK;
 }
 
 int phase_topup(mpb_handle* h, int pa, cudaStream_t s, int64_t& launches) {
-    if (h->nmag == 0) return MPB_OK;
-    const Bufs b = make_bufs(h, pa);
-    k_llg_topup<<<(h->nmag + 255) / 256, 256, 0, s>>>(h->g, b, h->mats, ids_view(h),
-                                                      h->magcells, h->magowned, h->nmag,
-                                                      h->st);
-    ++launches;
-    return MPB_OK;
+    return h->f32 ? phase_topup_t<float>(h, pa, s, launches)
+                  : phase_topup_t<double>(h, pa, s, launches);
 }
 
 int phase_decide(mpb_handle* h, cudaStream_t s, int64_t& launches) {
@@ -377,20 +429,22 @@ int phase_decide(mpb_handle* h, cudaStream_t s, int64_t& launches) {
 }
 
 // after r* is settled: deferred E, x/y walls, z-wall fix-up, source + probes
-int phase_post(mpb_handle* h, int pa, cudaStream_t s, int64_t& launches,
-               bool esweep = true) {
+template <typename T>
+int phase_post_t(mpb_handle* h, int pa, cudaStream_t s, int64_t& launches, bool esweep) {
     const Geom& g = h->g;
-    const Bufs b = make_bufs(h, pa);
+    const BufsT<T> b = make_bufs<T>(h, pa);
     const uint8_t* ids = ids_view(h);
     if (h->variant != 1 && h->nmag > 0) {
         int rc = launch_deferred(h, g, b, s);
         if (rc) return rc;
         ++launches;
     }
-    if (h->variant == 1 && esweep) {
-        const dim3 plane_grid((g.FyFz + 255) / 256, g.c1 - g.c0);
-        k_esweep<<<plane_grid, 256, 0, s>>>(g, b, h->mats, ids, h->st);
-        ++launches;
+    if constexpr (sizeof(T) == 8) {
+        if (h->variant == 1 && esweep) {
+            const dim3 plane_grid((g.FyFz + 255) / 256, g.c1 - g.c0);
+            k_esweep<<<plane_grid, 256, 0, s>>>(g, b, h->mats, ids, h->st);
+            ++launches;
+        }
     }
     // x and y walls: one launch for the four faces (k_walls_xy); z walls
     // are in the sweep (+ k_zfix) or, unfused, one k_wall launch per face
@@ -404,7 +458,7 @@ int phase_post(mpb_handle* h, int pa, cudaStream_t s, int64_t& launches,
                                                       : (int64_t)(g.c1 - g.c0) * g.F[2]);
             }
         if (act && !h->wall_per_face) {
-            CU(launch_pdl(h->pdl, k_walls_xy, dim3((unsigned)((cnt + 255) / 256), 4), dim3(256),
+            CU(launch_pdl(h->pdl, k_walls_xy<T>, dim3((unsigned)((cnt + 255) / 256), 4), dim3(256),
                           s, g, b, (const mpb_material*)h->mats, ids, (const StepState*)h->st,
                           act));
             ++launches;
@@ -417,7 +471,8 @@ int phase_post(mpb_handle* h, int pa, cudaStream_t s, int64_t& launches,
         const int u = axis == 0 ? 1 : 0, w = axis == 2 ? 1 : 2;
         const int64_t nu = u == 0 ? g.c1 - g.c0 : g.F[u];
         const int64_t cnt = nu * g.F[w];
-        k_wall<<<(unsigned)((cnt + 255) / 256), 256, 0, s>>>(g, b, h->mats, ids, h->st, face);
+        k_wall<T><<<(unsigned)((cnt + 255) / 256), 256, 0, s>>>(g, b, h->mats, ids, h->st,
+                                                                face);
         ++launches;
     }
     if (g.zin) {
@@ -425,11 +480,17 @@ int phase_post(mpb_handle* h, int pa, cudaStream_t s, int64_t& launches,
         if (rc) return rc;
         launches += zfix_launches(h);
     }
-    CU(launch_pdl(h->pdl, k_finish, dim3(1), dim3(256), s, g, b, h->src,
+    CU(launch_pdl(h->pdl, k_finish<T>, dim3(1), dim3(256), s, g, b, h->src,
                   (const ProbeDesc*)h->probes, h->nprobes, 1 - pa,
                   h->any_magnetic ? 1 : 0, h->st));
     ++launches;
     return MPB_OK;
+}
+
+int phase_post(mpb_handle* h, int pa, cudaStream_t s, int64_t& launches,
+               bool esweep = true) {
+    return h->f32 ? phase_post_t<float>(h, pa, s, launches, esweep)
+                  : phase_post_t<double>(h, pa, s, launches, esweep);
 }
 
 // End of a slab step: the boundary planes of the new state (set 1 - pa)
@@ -485,7 +546,7 @@ int enqueue_step(mpb_handle* h, int pa, bool timed) {
         CU(cudaEventCreate(&ea));
         CU(cudaEventCreate(&eb));
         CU(cudaEventRecord(ea, s));
-        const Bufs b = make_bufs(h, pa);
+        const Bufs b = make_bufs<double>(h, pa);
         const dim3 plane_grid((g.FyFz + 255) / 256, g.c1 - g.c0);
         k_esweep<<<plane_grid, 256, 0, s>>>(g, b, h->mats, ids_view(h), h->st);
         CU(cudaEventRecord(eb, s));
@@ -508,9 +569,10 @@ int exchange_group(mpb_handle* const* hs, int n, int pb, cudaStream_t s) {
         mpb_handle* b = hs[r + 1];
         const Geom& ga = a->g;
         const Geom& gb = b->g;
-        const size_t bytes = (size_t)ga.PP * sizeof(double);
-        auto plane = [](mpb_handle* h, double* alloc, int i) {
-            return alloc + (int64_t)(i - h->lo) * h->g.PP;
+        const size_t bytes = (size_t)ga.PP * a->esz;           // an E/H plane
+        const size_t mbytes = (size_t)ga.PP * sizeof(double);  // an M plane
+        auto plane = [](mpb_handle* h, void* alloc, int i) {
+            return static_cast<char*>(alloc) + (int64_t)(i - h->lo) * h->g.PP * (int64_t)h->esz;
         };
         const int up_src = ga.c1 - 1;   // a's last owned plane -> b's low ghost
         const int dn_src = gb.c0;       // b's first owned plane -> a's high ghost
@@ -522,10 +584,11 @@ int exchange_group(mpb_handle* const* hs, int n, int pb, cudaStream_t s) {
                                bytes, cudaMemcpyDeviceToDevice, s));
             if (m_up)
                 CU(cudaMemcpyAsync(b->M[pb][c] + (int64_t)(up_src - gb.mx0) * gb.PP,
-                                   a->M[pb][c] + (int64_t)(up_src - ga.mx0) * ga.PP, bytes,
+                                   a->M[pb][c] + (int64_t)(up_src - ga.mx0) * ga.PP, mbytes,
                                    cudaMemcpyDeviceToDevice, s));
-            CU(cudaMemcpyAsync(plane(a, a->E[pb][c], dn_src), plane(b, b->E[pb][c], dn_src),
-                               bytes, cudaMemcpyDeviceToDevice, s));
+            if (c > 0)   // Ex of the high ghost plane is never read (see exchange)
+                CU(cudaMemcpyAsync(plane(a, a->E[pb][c], dn_src), plane(b, b->E[pb][c], dn_src),
+                                   bytes, cudaMemcpyDeviceToDevice, s));
         }
     }
     return MPB_OK;
@@ -606,10 +669,15 @@ int recover_suspended(mpb_handle* const* hs, int n, bool group, cudaStream_t s) 
     if ((rc = drain_exchange(h0, s))) return rc;
     for (int q = 0; q < n; ++q) {
         k_suspend_clear<<<1, 256, 0, s>>>(hs[q]->st, g.max_iters);
-        const Bufs b = make_bufs(hs[q], pa);
-        if (hs[q]->nmag)
-            k_llg_cont_init<<<(hs[q]->nmag + 255) / 256, 256, 0, s>>>(
-                hs[q]->g, b, hs[q]->magcells, hs[q]->nmag, MagScratch{hs[q]->scratch});
+        if (!hs[q]->nmag) continue;
+        const dim3 grid((hs[q]->nmag + 255) / 256);
+        const MagScratch scr{hs[q]->scratch};
+        if (hs[q]->f32)
+            k_llg_cont_init<float><<<grid, 256, 0, s>>>(hs[q]->g, make_bufs<float>(hs[q], pa),
+                                                        hs[q]->magcells, hs[q]->nmag, scr);
+        else
+            k_llg_cont_init<double><<<grid, 256, 0, s>>>(hs[q]->g, make_bufs<double>(hs[q], pa),
+                                                         hs[q]->magcells, hs[q]->nmag, scr);
     }
     CU(cudaGetLastError());
     std::vector<unsigned long long> hist((size_t)g.max_iters + 2, 0ull);
@@ -645,10 +713,16 @@ int recover_suspended(mpb_handle* const* hs, int n, bool group, cudaStream_t s) 
         return MPB_OK;   // the caller reads the failure record
     }
     for (int q = 0; q < n; ++q) {
-        const Bufs b = make_bufs(hs[q], pa);
-        k_llg_cont_write<<<(std::max(hs[q]->nmag, 1) + 255) / 256, 256, 0, s>>>(
-            hs[q]->g, b, hs[q]->magcells, hs[q]->magowned, hs[q]->nmag,
-            MagScratch{hs[q]->scratch}, hs[q]->st, rstar);
+        const dim3 grid((std::max(hs[q]->nmag, 1) + 255) / 256);
+        const MagScratch scr{hs[q]->scratch};
+        if (hs[q]->f32)
+            k_llg_cont_write<float><<<grid, 256, 0, s>>>(
+                hs[q]->g, make_bufs<float>(hs[q], pa), hs[q]->magcells, hs[q]->magowned,
+                hs[q]->nmag, scr, hs[q]->st, rstar);
+        else
+            k_llg_cont_write<double><<<grid, 256, 0, s>>>(
+                hs[q]->g, make_bufs<double>(hs[q], pa), hs[q]->magcells, hs[q]->magowned,
+                hs[q]->nmag, scr, hs[q]->st, rstar);
     }
     CU(cudaGetLastError());
     for (int q = 0; q < n; ++q)
@@ -748,15 +822,20 @@ int upload_probes(mpb_handle* h) {
         const int64_t f = (int64_t)L[1] * g.F[2] + L[2];
         ProbeDesc d{};
         const bool owned = L[0] >= g.c0 && L[0] < g.c1;   // other ranks report 0
+        auto fptr = [&](void* a) -> const void* {         // typed view of an E/H buffer
+            return h->f32 ? (const void*)fview<float>(a, h) : (const void*)fview<double>(a, h);
+        };
         if (!owned) {
             d.ptr0 = d.ptr1 = nullptr;
             d.constant = 0.0;
         } else if (comp < MPB_COMP_HX) {
-            d.ptr0 = view(h->E[0][comp], h); d.ptr1 = view(h->E[1][comp], h);
+            d.ptr0 = fptr(h->E[0][comp]); d.ptr1 = fptr(h->E[1][comp]);
             d.off = L[0] * g.PP + f;
+            d.f32 = h->f32;
         } else if (comp < MPB_COMP_MX) {
-            d.ptr0 = view(h->H[0][comp - 3], h); d.ptr1 = view(h->H[1][comp - 3], h);
+            d.ptr0 = fptr(h->H[0][comp - 3]); d.ptr1 = fptr(h->H[1][comp - 3]);
             d.off = L[0] * g.PP + f;
+            d.f32 = h->f32;
         } else if (L[0] >= g.mx0 && L[0] < g.mx1) {
             d.ptr0 = h->M[0][comp - 6]; d.ptr1 = h->M[1][comp - 6];
             d.off = (int64_t)(L[0] - g.mx0) * g.PP + f;
@@ -791,8 +870,11 @@ int launch_line(mpb_handle* h, int64_t nsteps) {
     const int pa = h->parity, pb = (int)((h->parity + nsteps) & 1);
     LineArgs a{};
     for (int c = 0; c < 3; ++c) {
-        a.E[c] = h->E[pa][c]; a.H[c] = h->H[pa][c]; a.M[c] = h->mplanes ? h->M[pa][c] : nullptr;
-        a.Eo[c] = h->E[pb][c]; a.Ho[c] = h->H[pb][c]; a.Mo[c] = h->mplanes ? h->M[pb][c] : nullptr;
+        // (the line kernel runs only in fp64 storage)
+        a.E[c] = static_cast<double*>(h->E[pa][c]); a.H[c] = static_cast<double*>(h->H[pa][c]);
+        a.M[c] = h->mplanes ? h->M[pa][c] : nullptr;
+        a.Eo[c] = static_cast<double*>(h->E[pb][c]); a.Ho[c] = static_cast<double*>(h->H[pb][c]);
+        a.Mo[c] = h->mplanes ? h->M[pb][c] : nullptr;
         a.src_pol[c] = h->src.pol[c];
     }
     a.ids = h->ids;
@@ -821,6 +903,8 @@ int create_body(const mpb_setup* su, mpb_handle* h, int nranks, int x_lo, int x_
     const int nx = su->n[0], ny = su->n[1], nz = su->n[2];
     h->device = su->device;
     h->variant = su->kernel_variant;
+    h->f32 = su->storage == MPB_STORAGE_F32;
+    h->esz = h->f32 ? sizeof(float) : sizeof(double);
     h->graph_steps = su->graph_steps > 0 ? su->graph_steps : kDefaultGraphSteps;
     if (nranks > 1) h->graph_steps = 1;   // NCCL steps are enqueued eagerly
     h->nranks = nranks;
@@ -925,8 +1009,8 @@ int create_body(const mpb_setup* su, mpb_handle* h, int nranks, int x_lo, int x_
     auto chk = [&](int r) { if (r && !rc) rc = r; };
     for (int p = 0; p < 2; ++p)
         for (int c = 0; c < 3; ++c) {
-            chk(dev_alloc(h, &h->E[p][c], (size_t)h->nloc));
-            chk(dev_alloc(h, &h->H[p][c], (size_t)h->nloc));
+            chk(field_alloc(h, &h->E[p][c], (size_t)h->nloc));
+            chk(field_alloc(h, &h->H[p][c], (size_t)h->nloc));
             chk(dev_alloc(h, &h->M[p][c], (size_t)(h->mplanes * g.PP)));
         }
     chk(dev_alloc(h, &h->ids, (size_t)h->nloc));
@@ -948,7 +1032,12 @@ int create_body(const mpb_setup* su, mpb_handle* h, int nranks, int x_lo, int x_
     // cooperative fixup grid (single rank): co-resident blocks only
     if (h->nmag && nranks == 1) {
         int per_sm = 0, sms = 0;
-        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_llg_fixup, 256, 0));
+        if (h->f32) {
+            CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_llg_fixup<float>, 256, 0));
+        } else {
+            CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_llg_fixup<double>, 256,
+                                                             0));
+        }
         CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
         const int need = (h->nmag + 255) / 256;
         h->fixup_blocks = std::max(1, std::min(need, per_sm * sms));
@@ -973,7 +1062,7 @@ int create_body(const mpb_setup* su, mpb_handle* h, int nranks, int x_lo, int x_
                             (size_t)g.F[2] + 16;
         int optin = 0;
         CU(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
-        if (want && h->nranks == 1 && h->variant == 0 && g.n[0] == 1 && g.n[1] == 1 &&
+        if (want && !h->f32 && h->nranks == 1 && h->variant == 0 && g.n[0] == 1 && g.n[1] == 1 &&
             g.act[2] && g.n[2] >= 2 && h->nmag <= kLineThreads &&
             need + 1024 <= (size_t)optin) {
             h->line = true;
@@ -1037,7 +1126,7 @@ int create_body(const mpb_setup* su, mpb_handle* h, int nranks, int x_lo, int x_
 extern "C" {
 
 const char* mpb_version(void) {
-    return "magphon_b200 0.2 sm_100a fp64 fmad=false nccl";
+    return "magphon_b200 0.3 sm_100a fp64 (+fp32 storage) fmad=false nccl";
 }
 
 const char* mpb_last_error(void) { return g_err.c_str(); }
@@ -1073,6 +1162,10 @@ int mpb_create(const mpb_setup* su, mpb_handle** out) {
         if (su->faces[f] == MPB_FACE_MUR1 && su->n[f >> 1] <= 1)
             return fail_msg(MPB_EINVAL, "MUR1 on collapsed axis face %d", f);
     }
+    if (su->storage != MPB_STORAGE_F64 && su->storage != MPB_STORAGE_F32)
+        return fail_msg(MPB_EINVAL, "bad storage mode %d", su->storage);
+    if (su->storage == MPB_STORAGE_F32 && su->kernel_variant != 0)
+        return fail_msg(MPB_EINVAL, "fp32 storage runs the fused sweep (variant 0) only");
     const int nranks = std::max(1, su->nranks);
     const int nx = su->n[0], ny = su->n[1], nz = su->n[2];
     const int x_lo = nranks == 1 ? 0 : su->x_lo;
@@ -1139,19 +1232,54 @@ int mpb_load_state(mpb_handle* h, const double* const fields[6], const double* m
     CU(cudaStreamSynchronize(h->stream));
     const size_t row = (size_t)g.FyFz * sizeof(double);
     const int nplanes = h->hi - h->lo;
-    const size_t whole = (size_t)nplanes * g.PP * sizeof(double);
-    for (int c = 0; c < 6; ++c) {
-        double* d0 = c < 3 ? h->E[0][c] : h->H[0][c - 3];
-        double* d1 = c < 3 ? h->E[1][c] : h->H[1][c - 3];
-        if (fields[c]) {   // upload once, replicate into the second buffer set
+    const size_t whole = (size_t)nplanes * g.PP * h->esz;
+    // fp32 storage: host doubles pass through a device staging buffer of
+    // whole planes (bounded, so C5-size slabs never need a second full copy)
+    const int batch = h->f32 ? (int)std::max<int64_t>(1, std::min<int64_t>(
+                                   nplanes, (64ll << 20) / (g.PP * (int64_t)sizeof(double))))
+                             : 0;
+    double* stage = nullptr;
+    if (h->f32) {   // the 2-D copies fill [0, FyFz) of each plane: pitch padding stays 0
+        CU(cudaMalloc(&stage, (size_t)batch * g.PP * sizeof(double)));
+        CU(cudaMemset(stage, 0, (size_t)batch * g.PP * sizeof(double)));
+    }
+    int rc = MPB_OK;
+    for (int c = 0; c < 6 && !rc; ++c) {
+        void* d0 = c < 3 ? h->E[0][c] : h->H[0][c - 3];
+        void* d1 = c < 3 ? h->E[1][c] : h->H[1][c - 3];
+        if (!fields[c]) {  // NULL: the component starts at zero
+            if (cudaMemset(d0, 0, whole) != cudaSuccess || cudaMemset(d1, 0, whole) != cudaSuccess)
+                rc = fail_msg(MPB_ECUDA, "cudaMemset failed");
+            continue;
+        }
+        if (!h->f32) {     // upload once, replicate into the second buffer set
             CU(cudaMemcpy2D(d0, g.PP * sizeof(double), fields[c], row, row, nplanes,
                             cudaMemcpyHostToDevice));
-            CU(cudaMemcpy(d1, d0, whole, cudaMemcpyDeviceToDevice));
-        } else {           // NULL: the component starts at zero
-            CU(cudaMemset(d0, 0, whole));
-            CU(cudaMemset(d1, 0, whole));
+        } else {
+            for (int p0 = 0; p0 < nplanes && !rc; p0 += batch) {
+                const int np = std::min(batch, nplanes - p0);
+                // on the handle's stream: a pageable H2D cudaMemcpy2D may return
+                // before its DMA lands, and the conversion must see the data
+                if (cudaMemcpy2DAsync(stage, g.PP * sizeof(double),
+                                      fields[c] + (size_t)p0 * g.FyFz, row, row, np,
+                                      cudaMemcpyHostToDevice, h->stream) != cudaSuccess) {
+                    rc = fail_msg(MPB_ECUDA, "staging upload failed");
+                    break;
+                }
+                k_convert<double, float><<<1184, 256, 0, h->stream>>>(
+                    stage, static_cast<float*>(d0) + (size_t)p0 * g.PP, (int64_t)np * g.PP);
+                if (cudaStreamSynchronize(h->stream) != cudaSuccess)
+                    rc = fail_msg(MPB_ECUDA, "fp32 conversion failed");
+            }
         }
+        if (!rc && cudaMemcpy(d1, d0, whole, cudaMemcpyDeviceToDevice) != cudaSuccess)
+            rc = fail_msg(MPB_ECUDA, "device copy failed");
     }
+    if (stage) cudaFree(stage);
+    if (rc) return rc;
+    // the device-to-device replicas above are asynchronous on the legacy
+    // stream; the handle's (non-blocking) stream must not start before them
+    CU(cudaStreamSynchronize(cudaStreamLegacy));
     const int ny = g.n[1], nz = g.n[2];
     const int ncl = h->chi - h->clo;
     {
@@ -1171,21 +1299,25 @@ int mpb_load_state(mpb_handle* h, const double* const fields[6], const double* m
             h->hostM.assign(m, m + total);
         }
     }
-    if (h->mplanes) {
-        std::vector<double> pk((size_t)(h->mplanes * g.PP), 0.0);
-        for (int c = 0; c < 3; ++c) {
-            for (int i = g.mx0; i < g.mx1; ++i)
-                for (int j = 0; j < ny; ++j)
-                    for (int k = 0; k < nz; ++k)
-                        pk[(size_t)((i - g.mx0) * g.PP + (int64_t)j * g.F[2] + k)] =
-                            m[(((size_t)c * ncl + (i - h->clo)) * ny + j) * nz + k];
-            for (int p = 0; p < 2; ++p)
-                CU(cudaMemcpy(h->M[p][c], pk.data(), pk.size() * sizeof(double),
-                              cudaMemcpyHostToDevice));
-        }
+    if (h->mplanes) {   // M planes, packed a bounded batch of planes at a time
+        const int mb = (int)std::max<int64_t>(1, std::min<int64_t>(
+            h->mplanes, (64ll << 20) / (g.PP * (int64_t)sizeof(double))));
+        std::vector<double> pk((size_t)mb * g.PP, 0.0);
+        for (int c = 0; c < 3; ++c)
+            for (int i0 = g.mx0; i0 < g.mx1; i0 += mb) {
+                const int np = std::min(mb, g.mx1 - i0);
+                for (int i = i0; i < i0 + np; ++i)
+                    for (int j = 0; j < ny; ++j)
+                        for (int k = 0; k < nz; ++k)
+                            pk[(size_t)((i - i0) * g.PP + (int64_t)j * g.F[2] + k)] =
+                                m[(((size_t)c * ncl + (i - h->clo)) * ny + j) * nz + k];
+                for (int p = 0; p < 2; ++p)
+                    CU(cudaMemcpy(h->M[p][c] + (size_t)(i0 - g.mx0) * g.PP, pk.data(),
+                                  (size_t)np * g.PP * sizeof(double), cudaMemcpyHostToDevice));
+            }
     }
     h->parity = 0;
-    int rc = upload_probes(h);
+    rc = upload_probes(h);
     if (rc) return rc;
     return reset_state(h);
 }
@@ -1199,28 +1331,52 @@ int mpb_save_state(mpb_handle* h, double* const fields[6], double* m) {
     const size_t row = (size_t)g.FyFz * sizeof(double);
     const int p = h->parity;
     const int nplanes = h->hi - h->lo;
-    for (int c = 0; c < 6; ++c) {
-        const double* src = c < 3 ? h->E[p][c] : h->H[p][c - 3];
-        CU(cudaMemcpy2D(fields[c], row, src, g.PP * sizeof(double), row, nplanes,
-                        cudaMemcpyDeviceToHost));
+    const int batch = h->f32 ? (int)std::max<int64_t>(1, std::min<int64_t>(
+                                   nplanes, (64ll << 20) / (g.PP * (int64_t)sizeof(double))))
+                             : 0;
+    double* stage = nullptr;
+    if (h->f32) CU(cudaMalloc(&stage, (size_t)batch * g.PP * sizeof(double)));
+    int rc = MPB_OK;
+    for (int c = 0; c < 6 && !rc; ++c) {
+        const void* src = c < 3 ? h->E[p][c] : h->H[p][c - 3];
+        if (!h->f32) {
+            CU(cudaMemcpy2D(fields[c], row, src, g.PP * sizeof(double), row, nplanes,
+                            cudaMemcpyDeviceToHost));
+            continue;
+        }
+        for (int p0 = 0; p0 < nplanes && !rc; p0 += batch) {   // widen, then download
+            const int np = std::min(batch, nplanes - p0);
+            k_convert<float, double><<<1184, 256, 0, h->stream>>>(
+                static_cast<const float*>(src) + (size_t)p0 * g.PP, stage, (int64_t)np * g.PP);
+            if (cudaStreamSynchronize(h->stream) != cudaSuccess ||
+                cudaMemcpy2D(fields[c] + (size_t)p0 * g.FyFz, row, stage, g.PP * sizeof(double),
+                             row, np, cudaMemcpyDeviceToHost) != cudaSuccess)
+                rc = fail_msg(MPB_ECUDA, "staging download failed");
+        }
     }
+    if (stage) cudaFree(stage);
+    if (rc) return rc;
     const int ny = g.n[1], nz = g.n[2];
     const int ncl = h->chi - h->clo;
     if (h->hostM.empty())
         memset(m, 0, sizeof(double) * (size_t)3 * ncl * ny * nz);
     else
         memcpy(m, h->hostM.data(), h->hostM.size() * sizeof(double));
-    if (h->mplanes) {
-        std::vector<double> pk((size_t)(h->mplanes * g.PP));
-        for (int c = 0; c < 3; ++c) {
-            CU(cudaMemcpy(pk.data(), h->M[p][c], pk.size() * sizeof(double),
-                          cudaMemcpyDeviceToHost));
-            for (int i = g.mx0; i < g.mx1; ++i)
-                for (int j = 0; j < ny; ++j)
-                    for (int k = 0; k < nz; ++k)
-                        m[(((size_t)c * ncl + (i - h->clo)) * ny + j) * nz + k] =
-                            pk[(size_t)((i - g.mx0) * g.PP + (int64_t)j * g.F[2] + k)];
-        }
+    if (h->mplanes) {   // M planes, a bounded batch of planes at a time
+        const int mb = (int)std::max<int64_t>(1, std::min<int64_t>(
+            h->mplanes, (64ll << 20) / (g.PP * (int64_t)sizeof(double))));
+        std::vector<double> pk((size_t)mb * g.PP);
+        for (int c = 0; c < 3; ++c)
+            for (int i0 = g.mx0; i0 < g.mx1; i0 += mb) {
+                const int np = std::min(mb, g.mx1 - i0);
+                CU(cudaMemcpy(pk.data(), h->M[p][c] + (size_t)(i0 - g.mx0) * g.PP,
+                              (size_t)np * g.PP * sizeof(double), cudaMemcpyDeviceToHost));
+                for (int i = i0; i < i0 + np; ++i)
+                    for (int j = 0; j < ny; ++j)
+                        for (int k = 0; k < nz; ++k)
+                            m[(((size_t)c * ncl + (i - h->clo)) * ny + j) * nz + k] =
+                                pk[(size_t)((i - i0) * g.PP + (int64_t)j * g.F[2] + k)];
+            }
     }
     return MPB_OK;
 }
@@ -1449,23 +1605,29 @@ int mpb_total_energy(mpb_handle* h, double* out) {
     CU(cudaStreamSynchronize(h->stream));
     const Geom& g = h->g;
     const int p = h->parity;
-    const double* E[3];
-    const double* Hh[3];
-    const double* Mm[3];
+    const void* hp[9];
     for (int c = 0; c < 3; ++c) {
-        E[c] = view(h->E[p][c], h);
-        Hh[c] = view(h->H[p][c], h);
-        Mm[c] = h->M[p][c];
+        hp[c] = h->f32 ? (const void*)fview<float>(h->E[p][c], h)
+                       : (const void*)fview<double>(h->E[p][c], h);
+        hp[3 + c] = h->f32 ? (const void*)fview<float>(h->H[p][c], h)
+                           : (const void*)fview<double>(h->H[p][c], h);
+        hp[6 + c] = h->M[p][c];
     }
-    const double** dptr = nullptr;
-    CU(cudaMallocAsync(&dptr, 9 * sizeof(double*), h->stream));
-    const double* hp[9] = {E[0], E[1], E[2], Hh[0], Hh[1], Hh[2], Mm[0], Mm[1], Mm[2]};
+    const void** dptr = nullptr;
+    CU(cudaMallocAsync(&dptr, 9 * sizeof(void*), h->stream));
     CU(cudaMemcpyAsync(dptr, hp, sizeof hp, cudaMemcpyHostToDevice, h->stream));
     const int blocks = 1184;
     double* partial = nullptr;
     CU(cudaMallocAsync(&partial, 3 * blocks * sizeof(double), h->stream));
-    k_energy_partial<<<blocks, 256, 0, h->stream>>>(g, dptr, dptr + 3, dptr + 6, h->mats,
-                                                    ids_view(h), partial);
+    const double* const* dm = reinterpret_cast<const double* const*>(dptr + 6);
+    if (h->f32)
+        k_energy_partial<float><<<blocks, 256, 0, h->stream>>>(
+            g, reinterpret_cast<const float* const*>(dptr),
+            reinterpret_cast<const float* const*>(dptr + 3), dm, h->mats, ids_view(h), partial);
+    else
+        k_energy_partial<double><<<blocks, 256, 0, h->stream>>>(
+            g, reinterpret_cast<const double* const*>(dptr),
+            reinterpret_cast<const double* const*>(dptr + 3), dm, h->mats, ids_view(h), partial);
     CU(cudaGetLastError());
     std::vector<double> hpart((size_t)3 * blocks);
     CU(cudaMemcpyAsync(hpart.data(), partial, hpart.size() * sizeof(double),

@@ -20,9 +20,9 @@ struct FusedState {
 
 FusedState* fused_of(mpb_handle* h) { return reinterpret_cast<FusedState*>(h->fused); }
 
-template <int V, bool F3, int NT = kSweepThreads>
+template <int V, bool F3, int NT = kSweepThreads, typename T = double>
 int set_smem_attr(size_t smem) {
-    CU(cudaFuncSetAttribute(k_sweep<V, F3, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CU(cudaFuncSetAttribute(k_sweep<V, F3, NT, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)smem));
     return MPB_OK;
 }
@@ -45,12 +45,18 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
     sc.fz_magic = (uint32_t)(((1ull << 32) + Fz - 1) / Fz);
     if (Fz == 1) sc.fz_magic = 0;   // j = f for Fz == 1 handled below
     // staging ring bytes for a tile of T entries: 3 slots of E (T + both halo
-    // rows), H^n (T + low halo) and material ids
+    // rows), H^n (T + low halo) and material ids.  Field elements are esz
+    // bytes (8, or 4 in the fp32 storage mode); every staged run starts on a
+    // 16-byte boundary, i.e. a multiple of A entries.
+    const int esz = (int)h->esz;
+    const int A = 16 / esz;
+    // a staged run [a0, a1) spans at most its entries + 2(A-1): 2A of slack
+    auto cap_of = [&](int n) { return (n + 2 * A + A - 1) & ~(A - 1); };
     auto ring_bytes = [&](int T) {
-        const int ecap = (T + sc.hl + sc.eh + 4 + 1) & ~1;
-        const int hcap = (T + sc.hl + 4 + 1) & ~1;
+        const int ecap = cap_of(T + sc.hl + sc.eh);
+        const int hcap = cap_of(T + sc.hl);
         const int icap = T + sc.hl + 48;
-        return (size_t)kSlots * (((3 * ecap + 3 * hcap) * 8 + icap + 127) / 128 * 128);
+        return (size_t)kSlots * (((3 * ecap + 3 * hcap) * esz + icap + 127) / 128 * 128);
     };
     // Tile form, first that fits (V entries per thread, NT threads per CTA):
     //  * 3D planes of >= 8K entries: V=2, NT=256, two CTAs per SM (each one's
@@ -64,7 +70,8 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
     CU(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, h->device));
     CU(cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, h->device));
     cudaFuncAttributes fa{};
-    CU(cudaFuncGetAttributes(&fa, k_sweep<2, true, 256>));
+    if (h->f32) { CU(cudaFuncGetAttributes(&fa, k_sweep<2, true, 256, float>)); }
+    else        { CU(cudaFuncGetAttributes(&fa, k_sweep<2, true, 256>)); }
     const size_t fixed = fa.sharedSizeBytes + (size_t)reserved;
     const bool f3 = g.act[0] && g.act[1] && g.act[2];
     if (f3 && g.FyFz >= 2 * 256 * 16 && 2 * (ring_bytes(512) + fixed) <= (size_t)smem_sm) {
@@ -125,15 +132,15 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
         return waves * (1400.0 + T) * (((Fx + *nch - 1) / *nch) + 3.0);
     };
     sc.T = Tmax;
-    if (const char* e = getenv("MPB_SWEEP_T")) {   // even: 16-byte aligned tile starts
-        const int t = atoi(e) & ~1;
+    if (const char* e = getenv("MPB_SWEEP_T")) {   // multiple of A: 16-byte aligned tile starts
+        const int t = atoi(e) & ~(A - 1);
         if (t > 0 && t <= sc.T) sc.T = t;
     } else {
         int nch = 1;
         const double full = model(Tmax, &nch);
         double best = full;
         int bestT = Tmax;
-        for (int T = Tmax - 2; T >= Tmax / 2; T -= 2) {
+        for (int T = Tmax - A; T >= Tmax / 2; T -= A) {
             const double t = model(T, &nch);
             if (t < best - 1e-9) { best = t; bestT = T; }
         }
@@ -146,10 +153,10 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
             if (g.act[a] && !(g.d[a] >= 0x1p-40 && g.d[a] <= 0x1p10)) fastdiv = false;
         sc.fastdiv = fastdiv ? 1 : 0;
     }
-    sc.ecap = (sc.T + sc.hl + sc.eh + 4 + 1) & ~1;
-    sc.hcap = (sc.T + sc.hl + 4 + 1) & ~1;
+    sc.ecap = cap_of(sc.T + sc.hl + sc.eh);
+    sc.hcap = cap_of(sc.T + sc.hl);
     sc.icap = sc.T + sc.hl + 48;
-    sc.stage_bytes = ((3 * sc.ecap + 3 * sc.hcap) * 8 + sc.icap + 127) / 128 * 128;
+    sc.stage_bytes = ((3 * sc.ecap + 3 * sc.hcap) * esz + sc.icap + 127) / 128 * 128;
     fs->smem = (size_t)kSlots * sc.stage_bytes;
 
     const size_t static_smem = 8 * 1024;
@@ -172,15 +179,29 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
     fs->grid = sc.tiles * sc.nchunks;
     fs->F3 = g.act[0] && g.act[1] && g.act[2];
     int rc;
-    if (fs->NT == 256)
+    if (h->f32) {
+        if (fs->NT == 256)
+            rc = set_smem_attr<2, true, 256, float>(fs->smem);
+        else if (fs->F3)
+            rc = fs->V == 2 ? set_smem_attr<2, true, kSweepThreads, float>(fs->smem)
+                            : set_smem_attr<1, true, kSweepThreads, float>(fs->smem);
+        else
+            rc = fs->V == 2 ? set_smem_attr<2, false, kSweepThreads, float>(fs->smem)
+                            : set_smem_attr<1, false, kSweepThreads, float>(fs->smem);
+    } else if (fs->NT == 256) {
         rc = set_smem_attr<2, true, 256>(fs->smem);
-    else if (fs->F3)
+    } else if (fs->F3) {
         rc = fs->V == 2 ? set_smem_attr<2, true>(fs->smem) : set_smem_attr<1, true>(fs->smem);
-    else
+    } else {
         rc = fs->V == 2 ? set_smem_attr<2, false>(fs->smem) : set_smem_attr<1, false>(fs->smem);
+    }
     if (rc) return rc;
     {   // reciprocals of the spacings, computed once on the device
-        for (int a = 0; a < 3; ++a) sc.rd[a] = g.rd[a];   // set in mpb_create
+        for (int a = 0; a < 3; ++a) {
+            sc.rd[a] = g.rd[a];                        // set in mpb_create
+            sc.rdf[a] = (float)(1.0 / g.d[a]);         // fp32 storage mode
+        }
+        sc.coef_hf = (float)g.coef_h;
     }
     if (rc) return rc;
     // deferred E entries: {c, c+x, c+y, c+z} over magnetic cells
@@ -237,10 +258,11 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
     return MPB_OK;
 }
 
-int launch_zfix(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s) {
+template <typename T>
+int launch_zfix(mpb_handle* h, const Geom& g, const BufsT<T>& b, cudaStream_t s) {
     FusedState* fs = fused_of(h);
     if (!fs->nzlines) return MPB_OK;
-    CU(launch_pdl(h->pdl, k_zfix, dim3((fs->nzlines + 255) / 256), dim3(256), s, g, b,
+    CU(launch_pdl(h->pdl, k_zfix<T>, dim3((fs->nzlines + 255) / 256), dim3(256), s, g, b,
                   (const mpb_material*)h->mats, ids_view(h), (const int3*)fs->zlines,
                   fs->nzlines, (const StepState*)h->st));
     return MPB_OK;
@@ -249,10 +271,11 @@ int launch_zfix(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s) {
 int zfix_launches(mpb_handle* h) { return fused_of(h)->nzlines ? 1 : 0; }
 
 // LLG of the magnetic cells after the pure-Maxwell sweep (fused variant).
-int launch_llg_local(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s) {
+template <typename T>
+int launch_llg_local(mpb_handle* h, const Geom& g, const BufsT<T>& b, cudaStream_t s) {
     if (!h->nmag) return MPB_OK;
     const size_t smem = (size_t)(g.max_iters + 2) * sizeof(unsigned long long);
-    CU(launch_pdl_smem(h->pdl, k_llg_local, dim3((h->nmag + 255) / 256), dim3(256), smem, s,
+    CU(launch_pdl_smem(h->pdl, k_llg_local<T>, dim3((h->nmag + 255) / 256), dim3(256), smem, s,
                        g, b, (const mpb_material*)h->mats, ids_view(h),
                        (const int2*)h->magcells, (const unsigned char*)h->magowned, h->nmag,
                        h->st));
@@ -271,7 +294,8 @@ void destroy_fused(mpb_handle* h) {
 // part 0: every x-chunk; 1: the interior chunks (no ghost plane read or
 // written); 2: the first and last chunk (the only ones touching the ghost
 // planes a slab exchange fills).  Adds the launches made to `launches`.
-int launch_fused(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s, int part,
+template <typename T>
+int launch_fused(mpb_handle* h, const Geom& g, const BufsT<T>& b, cudaStream_t s, int part,
                  int64_t& launches) {
     FusedState* fs = fused_of(h);
     SweepCfg sc = fs->sc;
@@ -286,11 +310,12 @@ int launch_fused(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s, in
     }
     ++launches;
 #define MPB_LAUNCH(VV, FF)                                                              \
-    CU(launch_pdl_smem(h->pdl, k_sweep<VV, FF>, dim3(grid), dim3(kSweepThreads), fs->smem, s,  \
-                       g, b, (const mpb_material*)h->mats, ids_view(h), h->st, sc))
+    CU(launch_pdl_smem(h->pdl, k_sweep<VV, FF, kSweepThreads, T>, dim3(grid),              \
+                       dim3(kSweepThreads), fs->smem, s, g, b, (const mpb_material*)h->mats,  \
+                       ids_view(h), h->st, sc))
     if (fs->NT == 256) {
-        CU(launch_pdl_smem(h->pdl, k_sweep<2, true, 256>, dim3(grid), dim3(256), fs->smem, s, g,
-                           b, (const mpb_material*)h->mats, ids_view(h), h->st, sc));
+        CU(launch_pdl_smem(h->pdl, k_sweep<2, true, 256, T>, dim3(grid), dim3(256), fs->smem,
+                           s, g, b, (const mpb_material*)h->mats, ids_view(h), h->st, sc));
     } else if (fs->F3) {
         if (fs->V == 2) MPB_LAUNCH(2, true);
         else MPB_LAUNCH(1, true);
@@ -302,10 +327,11 @@ int launch_fused(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s, in
     return MPB_OK;
 }
 
-int launch_deferred(mpb_handle* h, const Geom& g, const Bufs& b, cudaStream_t s) {
+template <typename T>
+int launch_deferred(mpb_handle* h, const Geom& g, const BufsT<T>& b, cudaStream_t s) {
     FusedState* fs = fused_of(h);
     if (!fs->ndefer) return MPB_OK;
-    CU(launch_pdl(h->pdl, k_edefer, dim3((fs->ndefer + 255) / 256), dim3(256), s, g, b,
+    CU(launch_pdl(h->pdl, k_edefer<T>, dim3((fs->ndefer + 255) / 256), dim3(256), s, g, b,
                   (const mpb_material*)h->mats, ids_view(h), (const int2*)fs->defer,
                   fs->ndefer, (const StepState*)h->st, 1));
     return MPB_OK;

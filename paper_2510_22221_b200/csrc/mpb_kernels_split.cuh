@@ -110,11 +110,12 @@ __global__ void __launch_bounds__(256) k_hsweep(Geom g, Bufs b,
 struct E3 { double x, y, z; };
 
 // Plain E^{n+1} at one entry (no walls), reading the new H from b.Hb.
-__device__ __forceinline__ E3 e_plain_at(const Geom& g, const Bufs& b,
+template <typename T>
+__device__ __forceinline__ E3 e_plain_at(const Geom& g, const BufsT<T>& b,
                                          const mpb_material* __restrict__ mats,
                                          const uint8_t* __restrict__ ids, int i, int j, int k,
                                          int64_t o) {
-    const double* const* H = b.Hb;
+    T* const* H = b.Hb;
     double cx = 0.0, cy = 0.0, cz = 0.0;
     const int64_t sx = g.PP, sy = g.F[2];
     const bool p[6] = {g.faces[0] == MPB_FACE_PMC, g.faces[1] == MPB_FACE_PMC,
@@ -189,7 +190,8 @@ struct MagScratch {    // per magnetic cell, structure of arrays
     double* v;         // 12 * nmag: Hn[3] Mn[3] cE[3] Mr[3]
 };
 
-__global__ void __launch_bounds__(256) k_llg_fixup(Geom g, Bufs b,
+template <typename T>
+__global__ void __launch_bounds__(256) k_llg_fixup(Geom g, BufsT<T> b,
                                                    const mpb_material* __restrict__ mats,
                                                    const uint8_t* __restrict__ ids,
                                                    const int2* __restrict__ cells, int nmag,
@@ -315,7 +317,8 @@ __global__ void __launch_bounds__(256) k_llg_fixup(Geom g, Bufs b,
 // ---------------------------------------------------------------------------
 constexpr int kMpbSuspend = 4;   // StepState.fail_kind of a suspended step
 
-__global__ void __launch_bounds__(256) k_llg_topup(Geom g, Bufs b,
+template <typename T>
+__global__ void __launch_bounds__(256) k_llg_topup(Geom g, BufsT<T> b,
                                                    const mpb_material* __restrict__ mats,
                                                    const uint8_t* __restrict__ ids,
                                                    const int2* __restrict__ cells,
@@ -412,7 +415,8 @@ __global__ void k_llg_decide(Geom g, StepState* st) {
 
 // Lockstep continuation of a suspended multi-rank step (host-driven, one
 // iterate per launch).  Scratch per local cell: Hn[3] Mn[3] cE[3] Mr[3].
-__global__ void __launch_bounds__(256) k_llg_cont_init(Geom g, Bufs b,
+template <typename T>
+__global__ void __launch_bounds__(256) k_llg_cont_init(Geom g, BufsT<T> b,
                                                        const int2* __restrict__ cells, int n,
                                                        MagScratch scr) {
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
@@ -470,7 +474,8 @@ __global__ void __launch_bounds__(256) k_llg_cont_iter(Geom g,
 }
 
 // the settled iterate r*: H^{n+1} (every local cell) and M^{n+1} (owned)
-__global__ void __launch_bounds__(256) k_llg_cont_write(Geom g, Bufs b,
+template <typename T>
+__global__ void __launch_bounds__(256) k_llg_cont_write(Geom g, BufsT<T> b,
                                                         const int2* __restrict__ cells,
                                                         const unsigned char* __restrict__ owned,
                                                         int n, MagScratch scr, StepState* st,
@@ -505,7 +510,8 @@ __global__ void k_set_failure(StepState* st, double res, int it, int kind) {
 // MUR1 reads the pre-update planes straight from the read buffer Ea (the
 // reference copies them before the update, em.py:306-321).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_wall(Geom g, Bufs b,
+template <typename T>
+__global__ void __launch_bounds__(256) k_wall(Geom g, BufsT<T> b,
                                               const mpb_material* __restrict__ mats,
                                               const uint8_t* __restrict__ ids,
                                               const StepState* st, int face) {
@@ -546,7 +552,8 @@ __global__ void __launch_bounds__(256) k_wall(Geom g, Bufs b,
 // it).  Every other read is of entries no wall writes.  act: bit f = face f
 // active on this rank.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ double wall_value(const Geom& g, const Bufs& b,
+template <typename T>
+__device__ __forceinline__ double wall_value(const Geom& g, const BufsT<T>& b,
                                              const mpb_material* __restrict__ mats,
                                              const uint8_t* __restrict__ ids, int face, int c,
                                              int64_t ow, int64_t oi) {
@@ -556,7 +563,8 @@ __device__ __forceinline__ double wall_value(const Geom& g, const Bufs& b,
     return b.Ea[c][oi] + kk * (b.Eb[c][oi] - b.Ea[c][ow]);
 }
 
-__global__ void __launch_bounds__(256) k_walls_xy(Geom g, Bufs b,
+template <typename T>
+__global__ void __launch_bounds__(256) k_walls_xy(Geom g, BufsT<T> b,
                                                   const mpb_material* __restrict__ mats,
                                                   const uint8_t* __restrict__ ids,
                                                   const StepState* st, int act) {
@@ -602,13 +610,23 @@ __global__ void __launch_bounds__(256) k_walls_xy(Geom g, Bufs b,
     }
 }
 
+// Element-type conversion for fp32-storage uploads/downloads (round to
+// nearest; double -> float -> double is the identity on the stored values).
+template <typename Tin, typename Tout>
+__global__ void k_convert(const Tin* __restrict__ in, Tout* __restrict__ out, int64_t n) {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n;
+         q += (int64_t)gridDim.x * blockDim.x)
+        out[q] = (Tout)in[q];
+}
+
 // ---------------------------------------------------------------------------
 // Energy diagnostic (em.py:366-383): per-block partial sums in a fixed
 // order, then one block combines them -- deterministic run to run.
 // out[0..2] per block: sum eps E^2, sum H^2, sum M.Hbias.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_energy_partial(Geom g, const double* const* E,
-                                                        const double* const* H,
+template <typename T>
+__global__ void __launch_bounds__(256) k_energy_partial(Geom g, const T* const* E,
+                                                        const T* const* H,
                                                         const double* const* M,
                                                         const mpb_material* __restrict__ mats,
                                                         const uint8_t* __restrict__ ids,
@@ -622,9 +640,10 @@ __global__ void __launch_bounds__(256) k_energy_partial(Geom g, const double* co
         const int f = (int)(q - (int64_t)(i - g.c0) * g.FyFz);
         const int64_t o = i * g.PP + f;
         const mpb_material& m = mats[ids[o]];
-        se += m.eps * (E[0][o] * E[0][o]) + m.eps * (E[1][o] * E[1][o]) +
-              m.eps * (E[2][o] * E[2][o]);
-        sh += H[0][o] * H[0][o] + H[1][o] * H[1][o] + H[2][o] * H[2][o];
+        const double e0 = E[0][o], e1 = E[1][o], e2 = E[2][o];
+        const double h0 = H[0][o], h1 = H[1][o], h2 = H[2][o];
+        se += m.eps * (e0 * e0) + m.eps * (e1 * e1) + m.eps * (e2 * e2);
+        sh += h0 * h0 + h1 * h1 + h2 * h2;
         const int j = f / g.F[2], k = f - j * g.F[2];
         if (M[0] && i >= g.mx0 && i < g.mx1 && i < g.n[0] && j < g.n[1] && k < g.n[2]) {
             const int64_t om = (int64_t)(i - g.mx0) * g.PP + f;
@@ -652,7 +671,8 @@ struct SourceDesc {
     double pol[3];
 };
 
-__global__ void __launch_bounds__(256) k_finish(Geom g, Bufs b, SourceDesc src,
+template <typename T>
+__global__ void __launch_bounds__(256) k_finish(Geom g, BufsT<T> b, SourceDesc src,
                                                 const ProbeDesc* __restrict__ probes,
                                                 int nprobes, int parity_b, int record_iters,
                                                 StepState* st) {
@@ -665,14 +685,17 @@ __global__ void __launch_bounds__(256) k_finish(Geom g, Bufs b, SourceDesc src,
         for (int c = 0; c < 3; ++c)
             if (src.pol[c] != 0.0) {
                 const double pv = src.pol[c] * v;
-                b.Eb[c][src.off] = b.Eb[c][src.off] + pv;
+                b.Eb[c][src.off] = (double)b.Eb[c][src.off] + pv;
             }
     }
     __syncthreads();
     for (int p = threadIdx.x; p < nprobes; p += blockDim.x) {
         const ProbeDesc pd = probes[p];
-        const double* base = parity_b ? pd.ptr1 : pd.ptr0;
-        st->probe_out[row * nprobes + p] = base ? base[pd.off] : pd.constant;
+        const void* base = parity_b ? pd.ptr1 : pd.ptr0;
+        st->probe_out[row * nprobes + p] =
+            !base ? pd.constant
+                  : (pd.f32 ? (double)static_cast<const float*>(base)[pd.off]
+                            : static_cast<const double*>(base)[pd.off]);
     }
     for (int r = threadIdx.x; r <= g.max_iters + 1; r += blockDim.x) {
         st->hist[r] = 0ull;

@@ -106,6 +106,8 @@ struct SweepCfg {
     int nmat;           // entries of the material table
     int fastdiv;        // spacings within [2^-40, 2^10]: range-guarded divisions
     double rd[3];       // recip_of(d[a]) evaluated on the device at setup
+    float rdf[3];       // fp32 storage mode: 1/d[a] rounded to float
+    float coef_hf;      // fp32 storage mode: dt/mu0 rounded to float
 };
 
 __global__ void k_recips(double dx, double dy, double dz, double* out) {
@@ -165,13 +167,38 @@ __device__ __noinline__ Q6 slow_div6(double a0, double a1, double a2, double a3,
 // H^{n+1} at one entry of the staged plane (in place in shared memory).
 // Straight-line: all six differences and divisions are issued back to back
 // and the division guard is checked once for the batch.
+template <typename T>
 struct HCtx {
-    const double* Ex; const double* Ey; const double* Ez;
-    const double* Ey1; const double* Ez1;
-    double* Hx; double* Hy; double* Hz;
+    const T* Ex; const T* Ey; const T* Ez;
+    const T* Ey1; const T* Ez1;
+    T* Hx; T* Hy; T* Hz;
 };
 
-__device__ __forceinline__ void h_entry(const Geom& g, const HCtx& c, int e, int j, int k,
+// fp32 storage mode: the same stencil in float arithmetic, divisions by the
+// spacings as products with 1/d rounded to float (no bitwise contract: the
+// mode is checked against the fp64 oracle within a stated tolerance)
+__device__ __forceinline__ void h_entry_f32(const Geom& g, const HCtx<float>& c, int e, int j,
+                                            int k, bool cellplane, int Fz, float ry, float rz,
+                                            float rx, float& cx, float& cy, float& cz,
+                                            bool& vx, bool& vy, bool& vz, bool ax, bool ay,
+                                            bool az) {
+    vx = j < g.n[1] && k < g.n[2];
+    vy = cellplane && k < g.n[2];
+    vz = cellplane && j < g.n[1];
+    const float ex = c.Ex[e], ey = c.Ey[e], ez = c.Ez[e];
+    const float q0 = (c.Ez[e + Fz] - ez) * ry;   // dEz/dy
+    const float q1 = (c.Ex[e + Fz] - ex) * ry;   // dEx/dy
+    const float q2 = (c.Ey[e + 1] - ey) * rz;    // dEy/dz
+    const float q3 = (c.Ex[e + 1] - ex) * rz;    // dEx/dz
+    const float q4 = (c.Ez1[e] - ez) * rx;       // dEz/dx
+    const float q5 = (c.Ey1[e] - ey) * rx;       // dEy/dx
+    cx = 0.f; cy = 0.f; cz = 0.f;
+    if (ay) { cx = cx + q0; cz = cz - q1; }
+    if (az) { cx = cx - q2; cy = cy + q3; }
+    if (ax) { cy = cy - q4; cz = cz + q5; }
+}
+
+__device__ __forceinline__ void h_entry(const Geom& g, const HCtx<double>& c, int e, int j, int k,
                                         bool cellplane, int Fz, double ry, double rz,
                                         double rx, double& cx, double& cy, double& cz,
                                         bool& vx, bool& vy, bool& vz, bool g_fastdiv,
@@ -214,16 +241,18 @@ __device__ __forceinline__ void h_entry(const Geom& g, const HCtx& c, int e, int
     if (ax) { cy = cy - q4; cz = cz + q5; }
 }
 
-template <int V, bool F3, int NT = kSweepThreads>
+template <int V, bool F3, int NT = kSweepThreads, typename T = double>
 __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1)
-k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
+k_sweep(Geom g, BufsT<T> b, const mpb_material* __restrict__ mats,
         const uint8_t* __restrict__ gids, StepState* st, SweepCfg sc) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ uint64_t bars[kSlots];
+    constexpr bool kF32 = sizeof(T) == 4;
+    constexpr int A = 16 / (int)sizeof(T);   // entries per 16 bytes (TMA alignment)
 
-    __shared__ double s_cacb[MPB_MAX_MATERIALS * 2];
+    __shared__ T s_cacb[MPB_MAX_MATERIALS * 2];
 
-    __shared__ double s_murz[MPB_MAX_MATERIALS];
+    __shared__ T s_murz[MPB_MAX_MATERIALS];
     unsigned char* ring = smem;
 
     pdl_wait();   // launched behind the previous step's k_finish (see pdl_wait)
@@ -245,20 +274,20 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
     const int plast = (ax && i1 < Fx) ? i1 : i1 - 1;
     const int hlo = max(0, f0 - sc.hl);
     const int ehi = min(g.FyFz, f1 + sc.eh);
-    const int a0 = hlo & ~1;                         // 16-byte aligned starts
-    const int ae = (ehi + 1) & ~1;
-    const int ah = (f1 + 1) & ~1;
+    const int a0 = hlo & ~(A - 1);                   // 16-byte aligned starts
+    const int ae = (ehi + A - 1) & ~(A - 1);
+    const int ah = (f1 + A - 1) & ~(A - 1);
     const int ia0 = hlo & ~15;
     const int iae = min((f1 + 16) & ~15, (int)g.PP);   // +1: z1-wall neighbour id
-    const uint32_t ebytes = (uint32_t)(ae - a0) * 8u;
-    const uint32_t hbytes = (uint32_t)(ah - a0) * 8u;
+    const uint32_t ebytes = (uint32_t)(ae - a0) * (uint32_t)sizeof(T);
+    const uint32_t hbytes = (uint32_t)(ah - a0) * (uint32_t)sizeof(T);
     const uint32_t ibytes = (uint32_t)(iae - ia0);
-    const uint32_t hst_bytes = (uint32_t)(((f1 + 1) & ~1) - f0) * 8u;   // 16-byte multiple
+    const uint32_t hst_bytes = (uint32_t)(ah - f0) * (uint32_t)sizeof(T);   // 16-byte multiple
 
     for (int q = tid; q < sc.nmat; q += blockDim.x) {
-        s_cacb[2 * q] = mats[q].ca;
-        s_cacb[2 * q + 1] = mats[q].cb;
-        s_murz[q] = mats[q].mur_k[2];
+        s_cacb[2 * q] = (T)mats[q].ca;
+        s_cacb[2 * q + 1] = (T)mats[q].cb;
+        s_murz[q] = (T)mats[q].mur_k[2];
     }
     if (tid == 0) {
         for (int q = 0; q < kSlots; ++q) mbar_init(&bars[q], 1);
@@ -269,14 +298,14 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
     // slot layout: E[3][ecap] | H[3][hcap] | ids[icap]
     auto slot = [&](int p) { return (p - pstart) % kSlots; };
     auto sE = [&](int s, int c) {
-        return reinterpret_cast<double*>(ring + (size_t)s * sc.stage_bytes) + c * sc.ecap;
+        return reinterpret_cast<T*>(ring + (size_t)s * sc.stage_bytes) + c * sc.ecap;
     };
     auto sH = [&](int s, int c) {
-        return reinterpret_cast<double*>(ring + (size_t)s * sc.stage_bytes) +
+        return reinterpret_cast<T*>(ring + (size_t)s * sc.stage_bytes) +
                3 * sc.ecap + c * sc.hcap;
     };
     auto sI = [&](int s) {
-        return ring + (size_t)s * sc.stage_bytes + (3 * sc.ecap + 3 * sc.hcap) * 8;
+        return ring + (size_t)s * sc.stage_bytes + (3 * sc.ecap + 3 * sc.hcap) * sizeof(T);
     };
     auto issue = [&](int p) {   // issuing thread only
         const int s = slot(p);
@@ -305,6 +334,7 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
     // reciprocals of the spacings: recip_of() evaluated once at setup on the
     // device (identical bits); passing them keeps MUFU + 5 DFMA out of the loop
     const double rx = sc.rd[0], ry = sc.rd[1], rz = sc.rd[2];
+    const float rfx = sc.rdf[0], rfy = sc.rdf[1], rfz = sc.rdf[2];
     const int Fz = g.F[2];
     const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
     // collapsed axes: their (unused) quotients must not trip the guard
@@ -316,9 +346,9 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
     const bool pmc_y0 = g.faces[2] == MPB_FACE_PMC, pmc_y1 = g.faces[3] == MPB_FACE_PMC;
     const bool pmc_z0 = g.faces[4] == MPB_FACE_PMC, pmc_z1 = g.faces[5] == MPB_FACE_PMC;
 
-    double hy_prev[V], hz_prev[V];
+    T hy_prev[V], hz_prev[V];
 #pragma unroll
-    for (int v = 0; v < V; ++v) { hy_prev[v] = 0.0; hz_prev[v] = 0.0; }
+    for (int v = 0; v < V; ++v) { hy_prev[v] = T(0); hz_prev[v] = T(0); }
 
     for (int p = pstart; p <= i1 - 1; ++p) {
         const int s = slot(p);
@@ -328,8 +358,8 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
         // here): the only barrier per plane is the one between the phases
         mbar_wait(&bars[s], ((p - pstart) / kSlots) & 1);
         if (xnext) mbar_wait(&bars[s1], ((p + 1 - pstart) / kSlots) & 1);
-        HCtx hc{sE(s, 0), sE(s, 1), sE(s, 2), sE(s1, 1), sE(s1, 2),
-                sH(s, 0), sH(s, 1), sH(s, 2)};
+        HCtx<T> hc{sE(s, 0), sE(s, 1), sE(s, 2), sE(s1, 1), sE(s1, 2),
+                   sH(s, 0), sH(s, 1), sH(s, 2)};
         const unsigned char* ids = sI(s);
         const bool emit = p >= i0;
         const bool cellplane = p < nx || !ax;
@@ -339,15 +369,24 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
             const int j = fz_div((uint32_t)gg, sc.fz_magic);
             const int k = gg - j * Fz;
             const int e = gg - a0;
-            double cx, cy, cz;
             bool vx, vy, vz;
-            h_entry(g, hc, e, j, k, cellplane, Fz, ry, rz, rx, cx, cy, cz, vx, vy, vz, fastdiv,
-                    ax, ay, az);
             // magnetic cells get the plain update here too; k_llg_local
             // replaces their H (and the E entries around them, k_edefer)
-            if (vx) hc.Hx[e] = hc.Hx[e] - g.coef_h * cx;
-            if (vy) hc.Hy[e] = hc.Hy[e] - g.coef_h * cy;
-            if (vz) hc.Hz[e] = hc.Hz[e] - g.coef_h * cz;
+            if constexpr (kF32) {
+                float cx, cy, cz;
+                h_entry_f32(g, hc, e, j, k, cellplane, Fz, rfy, rfz, rfx, cx, cy, cz, vx, vy,
+                            vz, ax, ay, az);
+                if (vx) hc.Hx[e] = hc.Hx[e] - sc.coef_hf * cx;
+                if (vy) hc.Hy[e] = hc.Hy[e] - sc.coef_hf * cy;
+                if (vz) hc.Hz[e] = hc.Hz[e] - sc.coef_hf * cz;
+            } else {
+                double cx, cy, cz;
+                h_entry(g, hc, e, j, k, cellplane, Fz, ry, rz, rx, cx, cy, cz, vx, vy, vz,
+                        fastdiv, ax, ay, az);
+                if (vx) hc.Hx[e] = hc.Hx[e] - g.coef_h * cx;
+                if (vy) hc.Hy[e] = hc.Hy[e] - g.coef_h * cy;
+                if (vz) hc.Hz[e] = hc.Hz[e] - g.coef_h * cz;
+            }
         }
         // H^{n+1}(p) complete everywhere, and every thread is past E(p-1) and
         // H(p), the last readers of plane p-1's slot: refill it with p+2
@@ -373,66 +412,74 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
         }
 
         // ---- E^{n+1}(p, f) for the owned range ------------------------------
-        const double* Hx = hc.Hx;
-        const double* Hy = hc.Hy;
-        const double* Hz = hc.Hz;
+        const T* Hx = hc.Hx;
+        const T* Hy = hc.Hy;
+        const T* Hz = hc.Hz;
         const int64_t base = (int64_t)p * g.PP;
 #pragma unroll
         for (int v = 0; v < V; ++v) {
             const int f = f0 + tid + v * NT;
             if (f < f1) {
                 const int e = f - a0;
-                const double hx = Hx[e], hy = Hy[e], hz = Hz[e];
+                const T hx = Hx[e], hy = Hy[e], hz = Hz[e];
                 if (emit) {
                     const int j = fz_div((uint32_t)f, sc.fz_magic);
                     const int k = f - j * Fz;
                     const int ejm = j > 0 ? e - Fz : e;   // clamp: never read off-range
                     const int ekm = k > 0 ? e - 1 : e;
-                    const double hz_jm = Hz[ejm], hx_jm = Hx[ejm];
-                    const double hy_km = Hy[ekm], hx_km = Hx[ekm];
+                    const T hz_jm = Hz[ejm], hx_jm = Hx[ejm];
+                    const T hy_km = Hy[ekm], hx_km = Hx[ekm];
+                    const T zero = T(0);
                     // backward differences with PMC ghosts (em.py:185-203)
-                    const double zhi = (j == ny) ? (pmc_y1 ? -hz_jm : 0.0) : hz;
-                    const double zlo = (j == 0) ? (pmc_y0 ? -hz : 0.0) : hz_jm;
-                    const double xhi = (j == ny) ? (pmc_y1 ? -hx_jm : 0.0) : hx;
-                    const double xlo = (j == 0) ? (pmc_y0 ? -hx : 0.0) : hx_jm;
-                    const double yhi_k = (k == nz) ? (pmc_z1 ? -hy_km : 0.0) : hy;
-                    const double ylo_k = (k == 0) ? (pmc_z0 ? -hy : 0.0) : hy_km;
-                    const double xhi_k = (k == nz) ? (pmc_z1 ? -hx_km : 0.0) : hx;
-                    const double xlo_k = (k == 0) ? (pmc_z0 ? -hx : 0.0) : hx_km;
-                    const double zhi_i = (p == nx) ? (pmc_x1 ? -hz_prev[v] : 0.0) : hz;
-                    const double zlo_i = (p == 0) ? (pmc_x0 ? -hz : 0.0) : hz_prev[v];
-                    const double yhi_i = (p == nx) ? (pmc_x1 ? -hy_prev[v] : 0.0) : hy;
-                    const double ylo_i = (p == 0) ? (pmc_x0 ? -hy : 0.0) : hy_prev[v];
-                    const double b0 = zhi - zlo, b1 = xhi - xlo, b2 = yhi_k - ylo_k;
-                    const double b3 = xhi_k - xlo_k, b4 = zhi_i - zlo_i, b5 = yhi_i - ylo_i;
-                    unsigned gg2 = 0;
-                    double q0 = qdiv(b0, g.d[1], ry, gg2), q1 = qdiv(b1, g.d[1], ry, gg2);
-                    double q2 = qdiv(b2, g.d[2], rz, gg2), q3 = qdiv(b3, g.d[2], rz, gg2);
-                    double q4 = qdiv(b4, g.d[0], rx, gg2), q5 = qdiv(b5, g.d[0], rx, gg2);
-                    if (__builtin_expect(!fastdiv || gg2 > kGuardSpan, 0)) {
-                        const bool fine = fastdiv && in_range_or_zero(b0) &&
-                                          in_range_or_zero(b1) && in_range_or_zero(b2) &&
-                                          in_range_or_zero(b3) && in_range_or_zero(b4) &&
-                                          in_range_or_zero(b5);
-                        if (!fine) {
-                            const Q6 o = slow_div6(b0, b1, b2, b3, b4, b5, g.d[0], g.d[1],
-                                                   g.d[2], rx, ry, rz);
-                            q0 = o.q0; q1 = o.q1; q2 = o.q2; q3 = o.q3; q4 = o.q4; q5 = o.q5;
+                    const T zhi = (j == ny) ? (pmc_y1 ? -hz_jm : zero) : hz;
+                    const T zlo = (j == 0) ? (pmc_y0 ? -hz : zero) : hz_jm;
+                    const T xhi = (j == ny) ? (pmc_y1 ? -hx_jm : zero) : hx;
+                    const T xlo = (j == 0) ? (pmc_y0 ? -hx : zero) : hx_jm;
+                    const T yhi_k = (k == nz) ? (pmc_z1 ? -hy_km : zero) : hy;
+                    const T ylo_k = (k == 0) ? (pmc_z0 ? -hy : zero) : hy_km;
+                    const T xhi_k = (k == nz) ? (pmc_z1 ? -hx_km : zero) : hx;
+                    const T xlo_k = (k == 0) ? (pmc_z0 ? -hx : zero) : hx_km;
+                    const T zhi_i = (p == nx) ? (pmc_x1 ? -hz_prev[v] : zero) : hz;
+                    const T zlo_i = (p == 0) ? (pmc_x0 ? -hz : zero) : hz_prev[v];
+                    const T yhi_i = (p == nx) ? (pmc_x1 ? -hy_prev[v] : zero) : hy;
+                    const T ylo_i = (p == 0) ? (pmc_x0 ? -hy : zero) : hy_prev[v];
+                    const T b0 = zhi - zlo, b1 = xhi - xlo, b2 = yhi_k - ylo_k;
+                    const T b3 = xhi_k - xlo_k, b4 = zhi_i - zlo_i, b5 = yhi_i - ylo_i;
+                    T q0, q1, q2, q3, q4, q5;
+                    if constexpr (kF32) {
+                        q0 = b0 * rfy; q1 = b1 * rfy; q2 = b2 * rfz;
+                        q3 = b3 * rfz; q4 = b4 * rfx; q5 = b5 * rfx;
+                    } else {
+                        unsigned gg2 = 0;
+                        q0 = qdiv(b0, g.d[1], ry, gg2); q1 = qdiv(b1, g.d[1], ry, gg2);
+                        q2 = qdiv(b2, g.d[2], rz, gg2); q3 = qdiv(b3, g.d[2], rz, gg2);
+                        q4 = qdiv(b4, g.d[0], rx, gg2); q5 = qdiv(b5, g.d[0], rx, gg2);
+                        if (__builtin_expect(!fastdiv || gg2 > kGuardSpan, 0)) {
+                            const bool fine = fastdiv && in_range_or_zero(b0) &&
+                                              in_range_or_zero(b1) && in_range_or_zero(b2) &&
+                                              in_range_or_zero(b3) && in_range_or_zero(b4) &&
+                                              in_range_or_zero(b5);
+                            if (!fine) {
+                                const Q6 o = slow_div6(b0, b1, b2, b3, b4, b5, g.d[0], g.d[1],
+                                                       g.d[2], rx, ry, rz);
+                                q0 = o.q0; q1 = o.q1; q2 = o.q2; q3 = o.q3; q4 = o.q4;
+                                q5 = o.q5;
+                            }
                         }
                     }
-                    double cx = 0.0, cy = 0.0, cz = 0.0;   // em.py:217-231 order
+                    T cx = zero, cy = zero, cz = zero;   // em.py:217-231 order
                     if (ay) { cx = cx + q0; cz = cz - q1; }
                     if (az) { cx = cx - q2; cy = cy + q3; }
                     if (ax) { cy = cy - q4; cz = cz + q5; }
                     const int id = ids[f - ia0];
-                    const double ca = s_cacb[2 * id], cb = s_cacb[2 * id + 1];
-                    const double* Ex = hc.Ex;
-                    const double* Ey = hc.Ey;
-                    const double* Ez = hc.Ez;
-                    const double exa = Ex[e], eya = Ey[e];
-                    const double w0 = ca * (cx - cb * exa);
-                    const double w1 = ca * (cy - cb * eya);
-                    const double w2 = ca * (cz - cb * Ez[e]);
+                    const T ca = s_cacb[2 * id], cb = s_cacb[2 * id + 1];
+                    const T* Ex = hc.Ex;
+                    const T* Ey = hc.Ey;
+                    const T* Ez = hc.Ez;
+                    const T exa = Ex[e], eya = Ey[e];
+                    const T w0 = ca * (cx - cb * exa);
+                    const T w1 = ca * (cy - cb * eya);
+                    const T w2 = ca * (cz - cb * Ez[e]);
                     const uint32_t o = (uint32_t)base + (uint32_t)f;
                     // z walls (em.py:336-359) in the sweep: the owner of the inner
                     // entry (k=1 / k=nz-1) writes the tangential wall value; lines
@@ -446,14 +493,14 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
                     if (wy) b.Eb[1][o] = w1;
                     b.Eb[2][o] = w2;
                     if (zw0 && k == 1) {
-                        const double kk = s_murz[ids[f - 1 - ia0]];
-                        if (zx) b.Eb[0][o - 1] = z0pec ? 0.0 : exa + kk * (w0 - Ex[e - 1]);
-                        if (zy) b.Eb[1][o - 1] = z0pec ? 0.0 : eya + kk * (w1 - Ey[e - 1]);
+                        const T kk = s_murz[ids[f - 1 - ia0]];
+                        if (zx) b.Eb[0][o - 1] = z0pec ? zero : exa + kk * (w0 - Ex[e - 1]);
+                        if (zy) b.Eb[1][o - 1] = z0pec ? zero : eya + kk * (w1 - Ey[e - 1]);
                     }
                     if (zw1 && k == nz - 1) {
-                        const double kk = s_murz[ids[f + 1 - ia0]];
-                        if (zx) b.Eb[0][o + 1] = z1pec ? 0.0 : exa + kk * (w0 - Ex[e + 1]);
-                        if (zy) b.Eb[1][o + 1] = z1pec ? 0.0 : eya + kk * (w1 - Ey[e + 1]);
+                        const T kk = s_murz[ids[f + 1 - ia0]];
+                        if (zx) b.Eb[0][o + 1] = z1pec ? zero : exa + kk * (w0 - Ex[e + 1]);
+                        if (zy) b.Eb[1][o + 1] = z1pec ? zero : eya + kk * (w1 - Ey[e + 1]);
                     }
                     if constexpr (!kBulkH) {
                         const bool cp = p < nx || !ax;
@@ -488,7 +535,8 @@ k_sweep(Geom g, Bufs b, const mpb_material* __restrict__ mats,
 #ifndef MPB_LLG_MINB
 #define MPB_LLG_MINB 3
 #endif
-__global__ void __launch_bounds__(256, MPB_LLG_MINB) k_llg_local(Geom g, Bufs b,
+template <typename T>
+__global__ void __launch_bounds__(256, MPB_LLG_MINB) k_llg_local(Geom g, BufsT<T> b,
                                                    const mpb_material* __restrict__ mats,
                                                    const uint8_t* __restrict__ ids,
                                                    const int2* __restrict__ cells,
@@ -538,7 +586,8 @@ __global__ void __launch_bounds__(256, MPB_LLG_MINB) k_llg_local(Geom g, Bufs b,
 // E entries whose curl-H stencil touches a magnetic H entry, recomputed after
 // the LLG fixup settled r* (only when the fixup had to recompute).  Uses the
 // sweep's z-wall write rules so the in-sweep z walls stay consistent.
-__global__ void __launch_bounds__(256) k_edefer(Geom g, Bufs b,
+template <typename T>
+__global__ void __launch_bounds__(256) k_edefer(Geom g, BufsT<T> b,
                                                 const mpb_material* __restrict__ mats,
                                                 const uint8_t* __restrict__ ids,
                                                 const int2* __restrict__ list, int n,
@@ -582,7 +631,8 @@ __global__ void __launch_bounds__(256) k_edefer(Geom g, Bufs b,
 // values) or write (post-x/y inner values).  Runs after the x/y wall
 // kernels, so the reference face order x0,x1,y0,y1,z0,z1 holds.
 // list entries: (comp, i, j) packed as int3.
-__global__ void __launch_bounds__(256) k_zfix(Geom g, Bufs b,
+template <typename T>
+__global__ void __launch_bounds__(256) k_zfix(Geom g, BufsT<T> b,
                                               const mpb_material* __restrict__ mats,
                                               const uint8_t* __restrict__ ids,
                                               const int3* __restrict__ lines, int n,

@@ -142,10 +142,16 @@ class DeviceRun:
 
     def __init__(self, grid, materials, boundaries, source_loc, source_pol,
                  probes, llg_params, dt: float, device: int = 0,
-                 kernel_variant: int = 0, graph_steps: int = 0, slab=None):
+                 kernel_variant: int = 0, graph_steps: int = 0, slab=None,
+                 storage: str = "f64"):
         """``slab``: None (whole grid on one GPU) or a ``parallel.Slab``
         (multi-rank x-slab); ``materials`` then covers the slab's cell
-        planes incl. ghosts (``Slab.cell_range``), ``grid`` is global."""
+        planes incl. ghosts (``Slab.cell_range``), ``grid`` is global.
+        ``storage``: "f64" (reference precision, bit-exact) or "f32" (E/H in
+        fp32 on the device, M and the LLG in fp64; within tolerance)."""
+        if storage not in N.STORAGE_CODES:
+            raise ValueError(f"storage must be one of {sorted(N.STORAGE_CODES)}")
+        self.storage = storage
         self.lib = N.load_library()
         self.grid = grid
         self.n = grid.cell_shape
@@ -186,6 +192,7 @@ class DeviceRun:
         su.device = device
         su.kernel_variant = kernel_variant
         su.graph_steps = graph_steps
+        su.storage = N.STORAGE_CODES[storage]
         n_magnetic = magnetic_count(materials)
         if slab is None:
             su.nranks, su.rank, su.x_lo, su.x_hi = 1, 0, 0, grid.nx

@@ -185,12 +185,15 @@ def _raise_failure(fail, config):
 
 
 def run(config: SimConfig, bias: float | None = None, resume: dict | None = None,
-        *, device: int = 0, kernel_variant: int = 0) -> RunResult:
+        *, device: int = 0, kernel_variant: int = 0, storage: str = "f64") -> RunResult:
     """Execute a full run on the GPU (reference sim.py:125-180).
 
     With ``bias`` the magnets' bias is overridden along
     ``config.bias_direction``; ``resume`` continues from a snapshot dict and
-    is bit-identical to an uninterrupted run.
+    is bit-identical to an uninterrupted run.  ``storage="f32"`` (not in the
+    reference API) keeps E and H in fp32 on the device -- half the HBM
+    traffic per step, M and the LLG still fp64 -- and agrees with the fp64
+    path within the tolerance tests/test_fp32_gpu.py states, not bitwise.
     """
     materials = config.materials if bias is None else _materials_with_bias(
         config.materials, bias, config.bias_direction)
@@ -214,7 +217,7 @@ def run(config: SimConfig, bias: float | None = None, resume: dict | None = None
         # step's LLG; with no step left to run it never reaches them
         pending = exc
     dev = _device_run(config, materials, keys, device=device, checked=pending is None,
-                      kernel_variant=kernel_variant)
+                      kernel_variant=kernel_variant, storage=storage)
     try:
         if resume is not None:
             st = resume["fields"]
