@@ -74,6 +74,8 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
     else        { CU(cudaFuncGetAttributes(&fa, k_sweep<2, true, 256>)); }
     const size_t fixed = fa.sharedSizeBytes + (size_t)reserved;
     const bool f3 = g.act[0] && g.act[1] && g.act[2];
+    // (fp32 storage: 1024-entry tiles in the two-CTA form, V = 4, measured
+    // 1.4% slower on C4 than the same 512-entry tiles; not used)
     if (f3 && g.FyFz >= 2 * 256 * 16 && 2 * (ring_bytes(512) + fixed) <= (size_t)smem_sm) {
         fs->V = 2; fs->NT = 256;
     } else if (g.FyFz >= 2 * kSweepThreads * 64 &&
