@@ -107,6 +107,17 @@ struct mpb_handle {
     double* d_probe = nullptr;
     int* d_iters = nullptr;
     int64_t stage_cap = 0;
+    // mpb_run, single rank: two staging sets (device + pinned host) so chunk
+    // c+1 runs while chunk c's probes / r* are copied out (double buffering)
+    struct RunStage {
+        double* d_src = nullptr; double* d_probe = nullptr; int* d_iters = nullptr;
+        double* h_src = nullptr; double* h_probe = nullptr; int* h_iters = nullptr;
+        StepState* h_st = nullptr;
+        cudaEvent_t done = nullptr;
+        int64_t s0 = 0, cnt = 0;
+        bool busy = false;
+    } rs[2];
+    int64_t rs_cap = 0;
     cudaStream_t stream = nullptr;
     cudaGraphExec_t graph[2] = {nullptr, nullptr};
     int64_t graph_launches[2] = {0, 0};   // kernels captured in each graph
@@ -133,6 +144,7 @@ struct mpb_handle {
     // timing
     int timing = 0;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events;
+    cudaEvent_t sweep_end = nullptr;   // timing: recorded right after the sweep launch
     double timed_ms = 0.0;
     int64_t timed_launches = 0;
     int64_t launches_last = 0;
@@ -344,6 +356,10 @@ int phase_sweep_t(mpb_handle* h, int pa, cudaStream_t s, int64_t& launches, int 
     }
     int rc = launch_fused(h, g, b, s, part, launches);
     if (rc) return rc;
+    if (h->sweep_end && part != 1) {   // kernel timing: the sweep alone, not the LLG
+        CU(cudaEventRecord(h->sweep_end, s));
+        h->sweep_end = nullptr;
+    }
     if (part != 1 && h->nmag > 0) {
         if ((rc = launch_llg_local(h, g, b, s))) return rc;
         ++launches;
@@ -521,10 +537,12 @@ int enqueue_step(mpb_handle* h, int pa, bool timed) {
         CU(cudaEventCreate(&e0));
         CU(cudaEventCreate(&e1));
         CU(cudaEventRecord(e0, s));
+        h->sweep_end = e1;
     }
     if ((rc = phase_sweep_overlapped(&h, 1, pa, s, launches))) return rc;
     if (timed) {
-        CU(cudaEventRecord(e1, s));
+        if (h->sweep_end) CU(cudaEventRecord(e1, s));   // split variant: after k_hsweep
+        h->sweep_end = nullptr;
         h->events.emplace_back(e0, e1);
     }
     if (h->nranks == 1) {
@@ -782,19 +800,45 @@ int enqueue_steps(mpb_handle* h, int64_t nsteps) {
     return drain_exchange(h, h->stream);
 }
 
+// Point the device bookkeeping at a run's staging buffers, stream-ordered
+// (a one-thread kernel: no host-side lifetime to wait for).
 int set_run_buffers(mpb_handle* h, int64_t n0, const double* src, double* probe,
                     int* iters) {
-    const long long step = n0, local = 0;
-    CU(cudaMemcpyAsync(&h->st->step, &step, sizeof step, cudaMemcpyHostToDevice, h->stream));
-    CU(cudaMemcpyAsync(&h->st->local, &local, sizeof local, cudaMemcpyHostToDevice,
-                       h->stream));
-    CU(cudaMemcpyAsync(&h->st->src_vals, &src, sizeof(void*), cudaMemcpyHostToDevice,
-                       h->stream));
-    CU(cudaMemcpyAsync(&h->st->probe_out, &probe, sizeof(void*), cudaMemcpyHostToDevice,
-                       h->stream));
-    CU(cudaMemcpyAsync(&h->st->iters_out, &iters, sizeof(void*), cudaMemcpyHostToDevice,
-                       h->stream));
-    CU(cudaStreamSynchronize(h->stream));   // host locals above must outlive the copies
+    k_set_run<<<1, 1, 0, h->stream>>>(h->st, (long long)n0, src, probe, iters);
+    CU(cudaGetLastError());
+    return MPB_OK;
+}
+
+void free_run_stages(mpb_handle* h) {
+    for (auto& r : h->rs) {
+        dev_free(h, r.d_src); dev_free(h, r.d_probe); dev_free(h, r.d_iters);
+        if (r.h_src) cudaFreeHost(r.h_src);
+        if (r.h_probe) cudaFreeHost(r.h_probe);
+        if (r.h_iters) cudaFreeHost(r.h_iters);
+        if (r.h_st) cudaFreeHost(r.h_st);
+        if (r.done) cudaEventDestroy(r.done);
+        r = mpb_handle::RunStage{};
+    }
+    h->rs_cap = 0;
+}
+
+int alloc_run_stages(mpb_handle* h, int64_t cap) {
+    if (cap <= h->rs_cap) return MPB_OK;
+    CU(cudaStreamSynchronize(h->stream));
+    free_run_stages(h);
+    const int np = std::max(1, h->nprobes);
+    for (auto& r : h->rs) {
+        int rc = dev_alloc(h, &r.d_src, (size_t)cap);
+        if (!rc) rc = dev_alloc(h, &r.d_probe, (size_t)(cap * np));
+        if (!rc) rc = dev_alloc(h, &r.d_iters, (size_t)cap);
+        if (rc) return rc;
+        CU(cudaMallocHost(&r.h_src, sizeof(double) * cap));
+        CU(cudaMallocHost(&r.h_probe, sizeof(double) * cap * np));
+        CU(cudaMallocHost(&r.h_iters, sizeof(int) * cap));
+        CU(cudaMallocHost(&r.h_st, sizeof(StepState)));
+        CU(cudaEventCreateWithFlags(&r.done, cudaEventDisableTiming));
+    }
+    h->rs_cap = cap;
     return MPB_OK;
 }
 
@@ -1213,6 +1257,7 @@ void mpb_destroy(mpb_handle* h) {
     dev_free(h, h->d_src);
     dev_free(h, h->d_probe);
     dev_free(h, h->d_iters);
+    free_run_stages(h);
     destroy_fused(h);
     if (h->stream) cudaStreamSynchronize(h->stream);
     if (h->comm_x) ncclCommDestroy(h->comm_x);
@@ -1402,13 +1447,11 @@ int mpb_run_device(mpb_handle* h, int64_t n0, int64_t nsteps, const double* d_sr
     return rc;
 }
 
-int mpb_run(mpb_handle* h, int64_t n0, int64_t nsteps, const double* src_vals,
-            double* probe_out, int32_t* iters_out, mpb_failure* fail) {
-    g_err.clear();
-    if (fail) { fail->step = -1; fail->residual = 0; fail->iterations = 0; fail->kind = 0; }
-    if (!h || nsteps < 0 || (nsteps && !src_vals))
-        return fail_msg(MPB_EINVAL, "bad arguments");
-    CU(cudaSetDevice(h->device));
+namespace {
+// Multi-rank mpb_run: one chunk at a time with a host check after each, so a
+// suspended step (kMpbSuspend) can be continued before the chunk goes on.
+int run_sync(mpb_handle* h, int64_t n0, int64_t nsteps, const double* src_vals,
+             double* probe_out, int32_t* iters_out, mpb_failure* fail) {
     const int64_t cap = std::min<int64_t>(std::max<int64_t>(nsteps, 1), kRunChunk);
     if (cap > h->stage_cap) {
         dev_free(h, h->d_src); dev_free(h, h->d_probe); dev_free(h, h->d_iters);
@@ -1463,6 +1506,82 @@ int mpb_run(mpb_handle* h, int64_t n0, int64_t nsteps, const double* src_vals,
     }
     h->launches_last = launches;
     return MPB_OK;
+}
+
+// Single rank: chunks are double-buffered.  Chunk c is enqueued (source
+// values staged through pinned memory, the steps, then its probes, r* and
+// the step state copied to pinned memory behind an event) before the host
+// waits for chunk c-1 and hands its rows to the caller, so the GPU never
+// idles on the host between chunks.  A failure found in chunk c-1 returns
+// after the stream drains (the later chunk's kernels were no-ops).
+int run_pipelined(mpb_handle* h, int64_t n0, int64_t nsteps, const double* src_vals,
+                  double* probe_out, int32_t* iters_out, mpb_failure* fail) {
+    const int64_t cap = std::min<int64_t>(std::max<int64_t>(nsteps, 1), kRunChunk);
+    int rc = alloc_run_stages(h, cap);
+    if (rc) return rc;
+    const int np = h->nprobes;
+    int64_t launches = 0;
+    auto harvest = [&](mpb_handle::RunStage& r) -> int {
+        CU(cudaEventSynchronize(r.done));
+        r.busy = false;
+        if (np && probe_out)
+            memcpy(probe_out + r.s0 * np, r.h_probe, sizeof(double) * r.cnt * np);
+        if (iters_out) memcpy(iters_out + r.s0, r.h_iters, sizeof(int) * r.cnt);
+        const StepState& st = *r.h_st;
+        if (st.fail) {
+            CU(cudaStreamSynchronize(h->stream));
+            for (auto& o : h->rs) o.busy = false;
+            if (fail) {
+                fail->step = st.fail_step; fail->residual = st.fail_res;
+                fail->iterations = st.fail_it; fail->kind = st.fail_kind;
+            }
+            return fail_msg(MPB_ESTEP, "LLG fixed point failed at step %lld",
+                            (long long)st.fail_step);
+        }
+        return MPB_OK;
+    };
+    int c = 0;
+    for (int64_t s0 = 0; s0 < nsteps; s0 += cap, ++c) {
+        mpb_handle::RunStage& r = h->rs[c & 1];
+        if (r.busy && (rc = harvest(r))) { h->launches_last = launches; return rc; }
+        const int64_t cnt = std::min(cap, nsteps - s0);
+        memcpy(r.h_src, src_vals + s0, sizeof(double) * cnt);
+        CU(cudaMemcpyAsync(r.d_src, r.h_src, sizeof(double) * cnt, cudaMemcpyHostToDevice,
+                           h->stream));
+        h->launches_last = 0;
+        if ((rc = set_run_buffers(h, n0 + s0, r.d_src, r.d_probe, r.d_iters))) return rc;
+        if ((rc = enqueue_steps(h, cnt))) return rc;
+        launches += h->launches_last;
+        if (np)
+            CU(cudaMemcpyAsync(r.h_probe, r.d_probe, sizeof(double) * cnt * np,
+                               cudaMemcpyDeviceToHost, h->stream));
+        CU(cudaMemcpyAsync(r.h_iters, r.d_iters, sizeof(int) * cnt, cudaMemcpyDeviceToHost,
+                           h->stream));
+        CU(cudaMemcpyAsync(r.h_st, h->st, sizeof(StepState), cudaMemcpyDeviceToHost,
+                           h->stream));
+        CU(cudaEventRecord(r.done, h->stream));
+        r.s0 = s0; r.cnt = cnt; r.busy = true;
+    }
+    // the older of the two outstanding chunks first
+    for (int k = 0; k < 2; ++k) {
+        mpb_handle::RunStage& r = h->rs[(c + k) & 1];
+        if (r.busy && (rc = harvest(r))) { h->launches_last = launches; return rc; }
+    }
+    h->launches_last = launches;
+    return MPB_OK;
+}
+
+}  // namespace
+
+int mpb_run(mpb_handle* h, int64_t n0, int64_t nsteps, const double* src_vals,
+            double* probe_out, int32_t* iters_out, mpb_failure* fail) {
+    g_err.clear();
+    if (fail) { fail->step = -1; fail->residual = 0; fail->iterations = 0; fail->kind = 0; }
+    if (!h || nsteps < 0 || (nsteps && !src_vals))
+        return fail_msg(MPB_EINVAL, "bad arguments");
+    CU(cudaSetDevice(h->device));
+    if (h->nranks > 1) return run_sync(h, n0, nsteps, src_vals, probe_out, iters_out, fail);
+    return run_pipelined(h, n0, nsteps, src_vals, probe_out, iters_out, fail);
 }
 
 int mpb_check_failure(mpb_handle* h, mpb_failure* fail) {
@@ -1557,6 +1676,8 @@ int mpb_group_run(mpb_handle* const* hs, int32_t n, int64_t n0, int64_t nsteps,
     for (int r = 0; r < n && !rc; ++r) {
         CU(cudaMalloc(&dprobe[(size_t)r], cnt * std::max(1, hs[r]->nprobes) * sizeof(double)));
         rc = set_run_buffers(hs[r], n0, dsrc, dprobe[(size_t)r], diters + r * cnt);
+        // (on rank r's own stream; the group steps on rank 0's)
+        if (!rc) CU(cudaStreamSynchronize(hs[r]->stream));
     }
     int64_t t = 0;
     while (t < nsteps && !rc) {

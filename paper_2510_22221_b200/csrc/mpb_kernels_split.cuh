@@ -493,6 +493,16 @@ __global__ void __launch_bounds__(256) k_llg_cont_write(Geom g, BufsT<T> b,
     }
 }
 
+// Start of a run chunk: absolute step, output row 0, staging pointers.
+__global__ void k_set_run(StepState* st, long long step, const double* src, double* probe,
+                          int* iters) {
+    st->step = step;
+    st->local = 0;
+    st->src_vals = src;
+    st->probe_out = probe;
+    st->iters_out = iters;
+}
+
 // Clear a suspension (and the lockstep history) before the host continues
 // the step; record a failure the host-driven continuation found.
 __global__ void k_suspend_clear(StepState* st, int max_iters) {
