@@ -10,6 +10,7 @@ struct FusedState {
     int V = 2;
     int NT = kSweepThreads;
     bool F3 = true;
+    bool pmc = true;          // some face is PMC (two-CTA form: else the PMC-free build)
     int grid = 0;
     size_t smem = 0;
     int2* defer = nullptr;
@@ -20,10 +21,10 @@ struct FusedState {
 
 FusedState* fused_of(mpb_handle* h) { return reinterpret_cast<FusedState*>(h->fused); }
 
-template <int V, bool F3, int NT = kSweepThreads, typename T = double>
+template <int V, bool F3, int NT = kSweepThreads, typename T = double, bool PMC = true>
 int set_smem_attr(size_t smem) {
-    CU(cudaFuncSetAttribute(k_sweep<V, F3, NT, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)smem));
+    CU(cudaFuncSetAttribute(k_sweep<V, F3, NT, T, PMC>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     return MPB_OK;
 }
 
@@ -180,10 +181,15 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
     sc.ch_step = 1;
     fs->grid = sc.tiles * sc.nchunks;
     fs->F3 = g.act[0] && g.act[1] && g.act[2];
+    for (int f = 0; f < 6; ++f) fs->pmc = f == 0 ? g.faces[f] == MPB_FACE_PMC
+                                                  : (fs->pmc || g.faces[f] == MPB_FACE_PMC);
+    if (const char* e = getenv("MPB_SWEEP_PMC"))   // 1: the generic build (A/B, tests)
+        if (atoi(e) == 1) fs->pmc = true;
     int rc;
     if (h->f32) {
         if (fs->NT == 256)
-            rc = set_smem_attr<2, true, 256, float>(fs->smem);
+            rc = fs->pmc ? set_smem_attr<2, true, 256, float>(fs->smem)
+                         : set_smem_attr<2, true, 256, float, false>(fs->smem);
         else if (fs->F3)
             rc = fs->V == 2 ? set_smem_attr<2, true, kSweepThreads, float>(fs->smem)
                             : set_smem_attr<1, true, kSweepThreads, float>(fs->smem);
@@ -191,7 +197,8 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
             rc = fs->V == 2 ? set_smem_attr<2, false, kSweepThreads, float>(fs->smem)
                             : set_smem_attr<1, false, kSweepThreads, float>(fs->smem);
     } else if (fs->NT == 256) {
-        rc = set_smem_attr<2, true, 256>(fs->smem);
+        rc = fs->pmc ? set_smem_attr<2, true, 256>(fs->smem)
+                     : set_smem_attr<2, true, 256, double, false>(fs->smem);
     } else if (fs->F3) {
         rc = fs->V == 2 ? set_smem_attr<2, true>(fs->smem) : set_smem_attr<1, true>(fs->smem);
     } else {
@@ -315,7 +322,11 @@ int launch_fused(mpb_handle* h, const Geom& g, const BufsT<T>& b, cudaStream_t s
     CU(launch_pdl_smem(h->pdl, k_sweep<VV, FF, kSweepThreads, T>, dim3(grid),              \
                        dim3(kSweepThreads), fs->smem, s, g, b, (const mpb_material*)h->mats,  \
                        ids_view(h), h->st, sc))
-    if (fs->NT == 256) {
+    if (fs->NT == 256 && !fs->pmc) {
+        CU(launch_pdl_smem(h->pdl, k_sweep<2, true, 256, T, false>, dim3(grid), dim3(256),
+                           fs->smem, s, g, b, (const mpb_material*)h->mats, ids_view(h), h->st,
+                           sc));
+    } else if (fs->NT == 256) {
         CU(launch_pdl_smem(h->pdl, k_sweep<2, true, 256, T>, dim3(grid), dim3(256), fs->smem,
                            s, g, b, (const mpb_material*)h->mats, ids_view(h), h->st, sc));
     } else if (fs->F3) {

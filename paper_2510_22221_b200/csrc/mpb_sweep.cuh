@@ -241,7 +241,10 @@ __device__ __forceinline__ void h_entry(const Geom& g, const HCtx<double>& c, in
     if (ax) { cy = cy - q4; cz = cz + q5; }
 }
 
-template <int V, bool F3, int NT = kSweepThreads, typename T = double>
+// PMC: some face is PMC (its ghost values enter the curl-H differences);
+// false removes the ghost selects from the E phase at compile time (grids
+// walled by PEC / MUR1 only, e.g. every benchmark configuration).
+template <int V, bool F3, int NT = kSweepThreads, typename T = double, bool PMC = true>
 __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1)
 k_sweep(Geom g, BufsT<T> b, const mpb_material* __restrict__ mats,
         const uint8_t* __restrict__ gids, StepState* st, SweepCfg sc) {
@@ -342,13 +345,34 @@ k_sweep(Geom g, BufsT<T> b, const mpb_material* __restrict__ mats,
     const bool zw0 = g.zin && az && g.faces[4] != MPB_FACE_PMC;
     const bool zw1 = g.zin && az && g.faces[5] != MPB_FACE_PMC;
     const bool z0pec = g.faces[4] == MPB_FACE_PEC, z1pec = g.faces[5] == MPB_FACE_PEC;
-    const bool pmc_x0 = g.faces[0] == MPB_FACE_PMC, pmc_x1 = g.faces[1] == MPB_FACE_PMC;
-    const bool pmc_y0 = g.faces[2] == MPB_FACE_PMC, pmc_y1 = g.faces[3] == MPB_FACE_PMC;
-    const bool pmc_z0 = g.faces[4] == MPB_FACE_PMC, pmc_z1 = g.faces[5] == MPB_FACE_PMC;
+    const bool pmc_x0 = PMC && g.faces[0] == MPB_FACE_PMC;
+    const bool pmc_x1 = PMC && g.faces[1] == MPB_FACE_PMC;
+    const bool pmc_y0 = PMC && g.faces[2] == MPB_FACE_PMC;
+    const bool pmc_y1 = PMC && g.faces[3] == MPB_FACE_PMC;
+    const bool pmc_z0 = PMC && g.faces[4] == MPB_FACE_PMC;
+    const bool pmc_z1 = PMC && g.faces[5] == MPB_FACE_PMC;
 
     T hy_prev[V], hz_prev[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) { hy_prev[v] = T(0); hz_prev[v] = T(0); }
+    // The E-phase entries of a thread are the same on every plane: in fp32
+    // their row / column tests are evaluated once, as bits, before the plane
+    // loop (+4% on C4: that kernel is issue-bound); fp64 keeps the direct
+    // per-plane comparisons (the extra registers cost it 4%)
+    constexpr unsigned kLive = 1u, kJ0 = 2u, kJn = 4u, kK0 = 8u, kKn = 16u, kK1 = 32u,
+                       kKn1 = 64u, kZx = 128u, kJlt = 256u, kKlt = 512u;
+    auto entry_flags = [&](int f) -> unsigned {
+        if (f >= f1) return 0u;
+        const int j = fz_div((uint32_t)f, sc.fz_magic);
+        const int k = f - j * Fz;
+        return kLive | (j == 0 ? kJ0 : 0u) | (j == ny ? kJn : 0u) | (k == 0 ? kK0 : 0u) |
+               (k == nz ? kKn : 0u) | (k == 1 ? kK1 : 0u) | (k == nz - 1 ? kKn1 : 0u) |
+               (!(ay && (j <= 1 || j >= ny - 1)) ? kZx : 0u) | (j < ny ? kJlt : 0u) |
+               (k < nz ? kKlt : 0u);
+    };
+    unsigned efl[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) efl[v] = kF32 ? entry_flags(f0 + tid + v * NT) : 0u;
 
     for (int p = pstart; p <= i1 - 1; ++p) {
         const int s = slot(p);
@@ -416,29 +440,43 @@ k_sweep(Geom g, BufsT<T> b, const mpb_material* __restrict__ mats,
         const T* Hy = hc.Hy;
         const T* Hz = hc.Hz;
         const int64_t base = (int64_t)p * g.PP;
+        const bool zy = !(ax && (p <= 1 || p >= nx - 1));   // (per plane)
 #pragma unroll
         for (int v = 0; v < V; ++v) {
             const int f = f0 + tid + v * NT;
-            if (f < f1) {
+            // the entry's row / column tests: fp32 from the precomputed bits,
+            // fp64 as direct comparisons
+            bool live, j0, jn, k0, kn, k1, kn1, zx, jlt, klt;
+            if constexpr (kF32) {
+                const unsigned fl = efl[v];
+                live = fl & kLive; j0 = fl & kJ0; jn = fl & kJn; k0 = fl & kK0; kn = fl & kKn;
+                k1 = fl & kK1; kn1 = fl & kKn1; zx = fl & kZx; jlt = fl & kJlt; klt = fl & kKlt;
+            } else {
+                live = f < f1;
+                const int j = fz_div((uint32_t)f, sc.fz_magic);
+                const int k = f - j * Fz;
+                j0 = j == 0; jn = j == ny; k0 = k == 0; kn = k == nz; k1 = k == 1;
+                kn1 = k == nz - 1; zx = !(ay && (j <= 1 || j >= ny - 1)); jlt = j < ny;
+                klt = k < nz;
+            }
+            if (live) {
                 const int e = f - a0;
                 const T hx = Hx[e], hy = Hy[e], hz = Hz[e];
                 if (emit) {
-                    const int j = fz_div((uint32_t)f, sc.fz_magic);
-                    const int k = f - j * Fz;
-                    const int ejm = j > 0 ? e - Fz : e;   // clamp: never read off-range
-                    const int ekm = k > 0 ? e - 1 : e;
+                    const int ejm = j0 ? e : e - Fz;      // clamp: never read off-range
+                    const int ekm = k0 ? e : e - 1;
                     const T hz_jm = Hz[ejm], hx_jm = Hx[ejm];
                     const T hy_km = Hy[ekm], hx_km = Hx[ekm];
                     const T zero = T(0);
                     // backward differences with PMC ghosts (em.py:185-203)
-                    const T zhi = (j == ny) ? (pmc_y1 ? -hz_jm : zero) : hz;
-                    const T zlo = (j == 0) ? (pmc_y0 ? -hz : zero) : hz_jm;
-                    const T xhi = (j == ny) ? (pmc_y1 ? -hx_jm : zero) : hx;
-                    const T xlo = (j == 0) ? (pmc_y0 ? -hx : zero) : hx_jm;
-                    const T yhi_k = (k == nz) ? (pmc_z1 ? -hy_km : zero) : hy;
-                    const T ylo_k = (k == 0) ? (pmc_z0 ? -hy : zero) : hy_km;
-                    const T xhi_k = (k == nz) ? (pmc_z1 ? -hx_km : zero) : hx;
-                    const T xlo_k = (k == 0) ? (pmc_z0 ? -hx : zero) : hx_km;
+                    const T zhi = jn ? (pmc_y1 ? -hz_jm : zero) : hz;
+                    const T zlo = j0 ? (pmc_y0 ? -hz : zero) : hz_jm;
+                    const T xhi = jn ? (pmc_y1 ? -hx_jm : zero) : hx;
+                    const T xlo = j0 ? (pmc_y0 ? -hx : zero) : hx_jm;
+                    const T yhi_k = kn ? (pmc_z1 ? -hy_km : zero) : hy;
+                    const T ylo_k = k0 ? (pmc_z0 ? -hy : zero) : hy_km;
+                    const T xhi_k = kn ? (pmc_z1 ? -hx_km : zero) : hx;
+                    const T xlo_k = k0 ? (pmc_z0 ? -hx : zero) : hx_km;
                     const T zhi_i = (p == nx) ? (pmc_x1 ? -hz_prev[v] : zero) : hz;
                     const T zlo_i = (p == 0) ? (pmc_x0 ? -hz : zero) : hz_prev[v];
                     const T yhi_i = (p == nx) ? (pmc_x1 ? -hy_prev[v] : zero) : hy;
@@ -485,39 +523,35 @@ k_sweep(Geom g, BufsT<T> b, const mpb_material* __restrict__ mats,
                     // entry (k=1 / k=nz-1) writes the tangential wall value; lines
                     // an x/y wall reads or writes are left to k_zfix (run after the
                     // x/y wall kernels, preserving the face order x0..z1)
-                    const bool zx = !(ay && (j <= 1 || j >= ny - 1));
-                    const bool zy = !(ax && (p <= 1 || p >= nx - 1));
                     bool wx = true, wy = true;
-                    if ((zw0 && k == 0) || (zw1 && k == nz)) { wx = !zx; wy = !zy; }
+                    if ((zw0 && k0) || (zw1 && kn)) { wx = !zx; wy = !zy; }
                     if (wx) b.Eb[0][o] = w0;
                     if (wy) b.Eb[1][o] = w1;
                     b.Eb[2][o] = w2;
-                    if (zw0 && k == 1) {
+                    if (zw0 && k1) {
                         const T kk = s_murz[ids[f - 1 - ia0]];
                         if (zx) b.Eb[0][o - 1] = z0pec ? zero : exa + kk * (w0 - Ex[e - 1]);
                         if (zy) b.Eb[1][o - 1] = z0pec ? zero : eya + kk * (w1 - Ey[e - 1]);
                     }
-                    if (zw1 && k == nz - 1) {
+                    if (zw1 && kn1) {
                         const T kk = s_murz[ids[f + 1 - ia0]];
                         if (zx) b.Eb[0][o + 1] = z1pec ? zero : exa + kk * (w0 - Ex[e + 1]);
                         if (zy) b.Eb[1][o + 1] = z1pec ? zero : eya + kk * (w1 - Ey[e + 1]);
                     }
                     if constexpr (!kBulkH) {
                         const bool cp = p < nx || !ax;
-                        if (j < ny && k < nz) b.Hb[0][o] = hx;
-                        if (cp && k < nz) b.Hb[1][o] = hy;
-                        if (cp && j < ny) b.Hb[2][o] = hz;
+                        if (jlt && klt) b.Hb[0][o] = hx;
+                        if (cp && klt) b.Hb[1][o] = hy;
+                        if (cp && jlt) b.Hb[2][o] = hz;
                     }
                 } else if (!kBulkH && p == g.c0 - 1) {
                     // low ghost plane of a slab: its H^{n+1} is read by k_edefer
                     // (x-backward difference at plane c0) before the exchange
                     // delivers the owner's copy (identical values)
-                    const int j = fz_div((uint32_t)f, sc.fz_magic);
-                    const int k = f - j * Fz;
                     const uint32_t o = (uint32_t)base + (uint32_t)f;
-                    if (j < ny && k < nz) b.Hb[0][o] = hx;
-                    if (k < nz) b.Hb[1][o] = hy;
-                    if (j < ny) b.Hb[2][o] = hz;
+                    if (jlt && klt) b.Hb[0][o] = hx;
+                    if (klt) b.Hb[1][o] = hy;
+                    if (jlt) b.Hb[2][o] = hz;
                 }
                 hy_prev[v] = hy;
                 hz_prev[v] = hz;
