@@ -167,6 +167,7 @@ int launch_zfix(mpb_handle* h, const Geom& g, const BufsT<T>& b, cudaStream_t s)
 int zfix_launches(mpb_handle* h);
 template <typename T>
 int launch_llg_local(mpb_handle* h, const Geom& g, const BufsT<T>& b, cudaStream_t s);
+
 const char* fused_kernel_name();
 void fused_form(mpb_handle* h, int32_t out[4]);
 }  // namespace

@@ -190,15 +190,14 @@ struct MagScratch {    // per magnetic cell, structure of arrays
     double* v;         // 12 * nmag: Hn[3] Mn[3] cE[3] Mr[3]
 };
 
+// The fixup proper, run by every block of a cooperative grid (k_llg_fixup,
+// and the merged tail k_post); returns in every block.
 template <typename T>
-__global__ void __launch_bounds__(256) k_llg_fixup(Geom g, BufsT<T> b,
-                                                   const mpb_material* __restrict__ mats,
-                                                   const uint8_t* __restrict__ ids,
-                                                   const int2* __restrict__ cells, int nmag,
-                                                   MagScratch scr, StepState* st) {
+__device__ void llg_fixup_grid(const Geom& g, const BufsT<T>& b,
+                               const mpb_material* __restrict__ mats,
+                               const uint8_t* __restrict__ ids, const int2* __restrict__ cells,
+                               int nmag, MagScratch scr, StepState* st) {
     __shared__ unsigned long long red[32];
-    pdl_wait();
-    pdl_trigger();
     if (st->fail) return;
     const int rmin = -st->rc_negmin, rmax = st->rc_max;
     if (rmin == rmax && rmax <= g.max_iters) {
@@ -297,6 +296,17 @@ __global__ void __launch_bounds__(256) k_llg_fixup(Geom g, BufsT<T> b,
         }
     }
     if (tid == 0) { st->rstar = rstar; st->fixup_ran = 1; }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_llg_fixup(Geom g, BufsT<T> b,
+                                                   const mpb_material* __restrict__ mats,
+                                                   const uint8_t* __restrict__ ids,
+                                                   const int2* __restrict__ cells, int nmag,
+                                                   MagScratch scr, StepState* st) {
+    pdl_wait();
+    pdl_trigger();
+    llg_fixup_grid(g, b, mats, ids, cells, nmag, scr, st);
 }
 
 // ---------------------------------------------------------------------------
@@ -573,18 +583,14 @@ __device__ __forceinline__ double wall_value(const Geom& g, const BufsT<T>& b,
     return b.Ea[c][oi] + kk * (b.Eb[c][oi] - b.Ea[c][ow]);
 }
 
+// One entry t of x/y wall `face` (active faces: bits of act).
 template <typename T>
-__global__ void __launch_bounds__(256) k_walls_xy(Geom g, BufsT<T> b,
-                                                  const mpb_material* __restrict__ mats,
-                                                  const uint8_t* __restrict__ ids,
-                                                  const StepState* st, int act) {
-    pdl_wait();
-    pdl_trigger();
-    const int face = blockIdx.y;
-    if (st->fail || !((act >> face) & 1)) return;
+__device__ __forceinline__ void wall_xy_entry(const Geom& g, const BufsT<T>& b,
+                                              const mpb_material* __restrict__ mats,
+                                              const uint8_t* __restrict__ ids, int act,
+                                              int face, int64_t t) {
     const int side = face & 1;
     const int Fz = g.F[2];
-    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (face < 2) {                            // x wall: entries (j, k), Ey and Ez
         if (t >= (int64_t)g.F[1] * Fz) return;
         const int j = (int)(t / Fz);
@@ -618,6 +624,18 @@ __global__ void __launch_bounds__(256) k_walls_xy(Geom g, BufsT<T> b,
             b.Eb[2][ow] = b.Ea[2][oi] + kk * (ez_in - b.Ea[2][ow]);
         }
     }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_walls_xy(Geom g, BufsT<T> b,
+                                                  const mpb_material* __restrict__ mats,
+                                                  const uint8_t* __restrict__ ids,
+                                                  const StepState* st, int act) {
+    pdl_wait();
+    pdl_trigger();
+    const int face = blockIdx.y;
+    if (st->fail || !((act >> face) & 1)) return;
+    wall_xy_entry(g, b, mats, ids, act, face, (int64_t)blockIdx.x * blockDim.x + threadIdx.x);
 }
 
 // Element-type conversion for fp32-storage uploads/downloads (round to
@@ -681,13 +699,11 @@ struct SourceDesc {
     double pol[3];
 };
 
+// Source, probes, r* record and the bookkeeping reset, by one block.
 template <typename T>
-__global__ void __launch_bounds__(256) k_finish(Geom g, BufsT<T> b, SourceDesc src,
-                                                const ProbeDesc* __restrict__ probes,
-                                                int nprobes, int parity_b, int record_iters,
-                                                StepState* st) {
-    pdl_wait();
-    pdl_trigger();
+__device__ void finish_block(const Geom& g, const BufsT<T>& b, const SourceDesc& src,
+                             const ProbeDesc* __restrict__ probes, int nprobes, int parity_b,
+                             int record_iters, StepState* st) {
     if (st->fail) return;
     const long long row = st->local;
     if (threadIdx.x == 0) {
@@ -720,6 +736,16 @@ __global__ void __launch_bounds__(256) k_finish(Geom g, BufsT<T> b, SourceDesc s
         st->local = row + 1;
         st->step = st->step + 1;
     }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_finish(Geom g, BufsT<T> b, SourceDesc src,
+                                                const ProbeDesc* __restrict__ probes,
+                                                int nprobes, int parity_b, int record_iters,
+                                                StepState* st) {
+    pdl_wait();
+    pdl_trigger();
+    finish_block(g, b, src, probes, nprobes, parity_b, record_iters, st);
 }
 
 }  // namespace mpb

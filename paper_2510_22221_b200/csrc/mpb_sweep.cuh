@@ -569,23 +569,15 @@ k_sweep(Geom g, BufsT<T> b, const mpb_material* __restrict__ mats,
 #ifndef MPB_LLG_MINB
 #define MPB_LLG_MINB 3
 #endif
+// One magnetic cell's fixed point to its local stop (CTA statistics in cs).
 template <typename T>
-__global__ void __launch_bounds__(256, MPB_LLG_MINB) k_llg_local(Geom g, BufsT<T> b,
-                                                   const mpb_material* __restrict__ mats,
-                                                   const uint8_t* __restrict__ ids,
-                                                   const int2* __restrict__ cells,
-                                                   const unsigned char* __restrict__ owned,
-                                                   int ncells, StepState* st) {
-    extern __shared__ unsigned long long lhist[];
-    __shared__ int lrc[2];
-    pdl_wait();
-    pdl_trigger();
-    if (st->fail) return;
-    CtaLlgStats cs{lhist, lrc};
-    cta_stats_init(cs, g.max_iters);
-    __syncthreads();
-    const int q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (q < ncells) {
+__device__ __forceinline__ void llg_local_cell(const Geom& g, const BufsT<T>& b,
+                                               const mpb_material* __restrict__ mats,
+                                               const uint8_t* __restrict__ ids,
+                                               const int2* __restrict__ cells,
+                                               const unsigned char* __restrict__ owned, int q,
+                                               CtaLlgStats& cs) {
+    {
         const int i = cells[q].x, f = cells[q].y;
         const int64_t o = i * g.PP + f;
         const int64_t om = (int64_t)(i - g.mx0) * g.PP + f;
@@ -613,6 +605,25 @@ __global__ void __launch_bounds__(256, MPB_LLG_MINB) k_llg_local(Geom g, BufsT<T
             atomicMax(&cs.rc[1], rc);
         }
     }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256, MPB_LLG_MINB) k_llg_local(Geom g, BufsT<T> b,
+                                                   const mpb_material* __restrict__ mats,
+                                                   const uint8_t* __restrict__ ids,
+                                                   const int2* __restrict__ cells,
+                                                   const unsigned char* __restrict__ owned,
+                                                   int ncells, StepState* st) {
+    extern __shared__ unsigned long long lhist[];
+    __shared__ int lrc[2];
+    pdl_wait();
+    pdl_trigger();
+    if (st->fail) return;
+    CtaLlgStats cs{lhist, lrc};
+    cta_stats_init(cs, g.max_iters);
+    __syncthreads();
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q < ncells) llg_local_cell(g, b, mats, ids, cells, owned, q, cs);
     __syncthreads();
     if (lrc[1] > 0) cta_stats_flush(cs, g.max_iters, st);
 }
@@ -620,17 +631,12 @@ __global__ void __launch_bounds__(256, MPB_LLG_MINB) k_llg_local(Geom g, BufsT<T
 // E entries whose curl-H stencil touches a magnetic H entry, recomputed after
 // the LLG fixup settled r* (only when the fixup had to recompute).  Uses the
 // sweep's z-wall write rules so the in-sweep z walls stay consistent.
+// One deferred E entry (the sweep's z-wall write rules).
 template <typename T>
-__global__ void __launch_bounds__(256) k_edefer(Geom g, BufsT<T> b,
-                                                const mpb_material* __restrict__ mats,
-                                                const uint8_t* __restrict__ ids,
-                                                const int2* __restrict__ list, int n,
-                                                const StepState* st, int always) {
-    pdl_wait();
-    pdl_trigger();
-    if (st->fail || (!always && !st->fixup_ran)) return;
-    const int q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= n) return;
+__device__ __forceinline__ void edefer_entry(const Geom& g, const BufsT<T>& b,
+                                             const mpb_material* __restrict__ mats,
+                                             const uint8_t* __restrict__ ids,
+                                             const int2* __restrict__ list, int q) {
     const int i = list[q].x, f = list[q].y;
     const int j = f / g.F[2];
     const int k = f - j * g.F[2];
@@ -660,22 +666,30 @@ __global__ void __launch_bounds__(256) k_edefer(Geom g, BufsT<T> b,
     }
 }
 
+template <typename T>
+__global__ void __launch_bounds__(256) k_edefer(Geom g, BufsT<T> b,
+                                                const mpb_material* __restrict__ mats,
+                                                const uint8_t* __restrict__ ids,
+                                                const int2* __restrict__ list, int n,
+                                                const StepState* st, int always) {
+    pdl_wait();
+    pdl_trigger();
+    if (st->fail || (!always && !st->fixup_ran)) return;
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q < n) edefer_entry(g, b, mats, ids, list, q);
+}
+
 // z walls on the lines the sweep leaves alone: Ex on rows j in {0,1,ny-1,ny}
 // and Ey on planes i in {0,1,nx-1,nx} -- the lines x/y walls read (pre-z
 // values) or write (post-x/y inner values).  Runs after the x/y wall
 // kernels, so the reference face order x0,x1,y0,y1,z0,z1 holds.
 // list entries: (comp, i, j) packed as int3.
+// One z-wall fix-up line entry (see k_zfix).
 template <typename T>
-__global__ void __launch_bounds__(256) k_zfix(Geom g, BufsT<T> b,
-                                              const mpb_material* __restrict__ mats,
-                                              const uint8_t* __restrict__ ids,
-                                              const int3* __restrict__ lines, int n,
-                                              const StepState* st) {
-    pdl_wait();
-    pdl_trigger();
-    if (st->fail) return;
-    const int q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= n) return;
+__device__ __forceinline__ void zfix_line(const Geom& g, const BufsT<T>& b,
+                                          const mpb_material* __restrict__ mats,
+                                          const uint8_t* __restrict__ ids,
+                                          const int3* __restrict__ lines, int q) {
     const int c = lines[q].x, i = lines[q].y, j = lines[q].z;
     const int64_t row = i * g.PP + (int64_t)j * g.F[2];
     const int nz = g.n[2];
@@ -689,6 +703,19 @@ __global__ void __launch_bounds__(256) k_zfix(Geom g, BufsT<T> b,
         if (g.faces[5] == MPB_FACE_PEC) b.Eb[c][ow] = 0.0;
         else b.Eb[c][ow] = b.Ea[c][oi] + mats[ids[ow]].mur_k[2] * (b.Eb[c][oi] - b.Ea[c][ow]);
     }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_zfix(Geom g, BufsT<T> b,
+                                              const mpb_material* __restrict__ mats,
+                                              const uint8_t* __restrict__ ids,
+                                              const int3* __restrict__ lines, int n,
+                                              const StepState* st) {
+    pdl_wait();
+    pdl_trigger();
+    if (st->fail) return;
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q < n) zfix_line(g, b, mats, ids, lines, q);
 }
 
 }  // namespace mpb
