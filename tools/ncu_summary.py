@@ -69,7 +69,7 @@ def raw_metrics(rep):
     return res
 
 
-def main(tag):
+def main(tag, dtype="f64"):
     PROF.mkdir(exist_ok=True)
     share = launches(tag)
     rep = OUT / f"sweep_{tag}.ncu-rep"
@@ -82,7 +82,9 @@ def main(tag):
             "smsp__average_warp_latency_issue_stalled_barrier",
             "lts__t_sector_hit_rate.pct", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"]
     lines = [f"# ncu summary -- k_sweep ({tag})", "",
-             "Command: `python bench.py --steps 6 --warmup 3 --no-cpu` (C4 1024x1024x128, fp64),",
+             f"Command: `python bench.py --steps 6 --warmup 3 --no-cpu"
+             f"{' --dtype f32' if dtype == 'f32' else ''}` (C4 1024x1024x128, "
+             f"{'fp64' if dtype == 'f64' else 'fp32 E/H storage'}),",
              "kernel launch #4 (after warm-up), `ncu --set full --clock-control none`.", "",
              "| metric | value |", "|---|---|"]
     for k in keys:
@@ -101,11 +103,11 @@ def main(tag):
         traffic = json.loads(tp.read_text())
     rb = m["dram__bytes_read.sum"][0]
     wb = m["dram__bytes_write.sum"][0]
-    traffic["k_sweep"] = rb + wb
-    traffic["_source"] = f"profiles/{tag}_sweep_summary.md (ncu --set full, one launch)"
+    traffic["k_sweep" if dtype == "f64" else f"k_sweep_{dtype}"] = rb + wb
+    traffic[f"_source_{dtype}"] = f"profiles/{tag}_sweep_summary.md (ncu --set full, one launch)"
     tp.write_text(json.dumps(traffic, indent=1) + "\n")
     print("\n".join(lines))
 
 
 if __name__ == "__main__":
-    main(sys.argv[1] if len(sys.argv) > 1 else "r01")
+    main(sys.argv[1] if len(sys.argv) > 1 else "r01", sys.argv[2] if len(sys.argv) > 2 else "f64")
