@@ -219,6 +219,16 @@ MPB_API int mpb_selftest_division(int32_t device, double d, const double* x, int
  * rounding (summation order differs), not bitwise. */
 MPB_API int mpb_total_energy(mpb_handle* h, double* out);
 
+/* Product with the Hankel data matrix X[t][a] = x[t+a] (t < n-columns+1,
+ * a < columns) of a probe series on the GPU: transpose = 0 computes
+ * out (M x r) = X in (columns x r), transpose = 1 computes out (columns x r)
+ * = X^T in (M x r); row-major host arrays, r <= 32.  The O(M columns r)
+ * work of the subspace mode extraction (reference analysis.esprit,
+ * analysis.py:64-115: SVD of the Hankel matrix), used by the randomized
+ * range finder in paper_2510_22221_b200/analysis.py; deterministic. */
+MPB_API int mpb_hankel_mul(int32_t device, const double* x, int64_t n, int32_t columns,
+                           int32_t r, int32_t transpose, const double* in, double* out);
+
 /* Multi-rank steps whose global residual went back above tol after the
  * last local stop and were continued in host-driven lockstep since the
  * handle was created (see mpb_failure.kind 4). */

@@ -62,7 +62,7 @@ EXPORTS = ("mpb_version", "mpb_last_error", "mpb_nccl_unique_id", "mpb_create", 
            "mpb_check_failure", "mpb_set_kernel_timing", "mpb_kernel_time",
            "mpb_launch_count", "mpb_device_bytes", "mpb_selftest_division",
            "mpb_group_run", "mpb_total_energy", "mpb_comm_info", "mpb_sweep_form",
-           "mpb_continued_steps")
+           "mpb_continued_steps", "mpb_hankel_mul")
 
 _lib = None
 
@@ -102,6 +102,8 @@ def load_library(path: os.PathLike | None = None) -> C.CDLL:
         "mpb_device_bytes": (C.c_int64, [C.c_void_p]),
         "mpb_total_energy": (C.c_int, [C.c_void_p, P(C.c_double)]),
         "mpb_continued_steps": (C.c_int64, [C.c_void_p]),
+        "mpb_hankel_mul": (C.c_int, [C.c_int32, P(C.c_double), C.c_int64, C.c_int32, C.c_int32,
+                                     C.c_int32, P(C.c_double), P(C.c_double)]),
         "mpb_sweep_form": (C.c_int, [C.c_void_p, P(C.c_int32)]),
         "mpb_comm_info": (C.c_int, [C.c_void_p, P(C.c_int32), P(C.c_int32), P(C.c_int32)]),
         "mpb_selftest_division": (C.c_int, [C.c_int32, C.c_double, P(C.c_double),

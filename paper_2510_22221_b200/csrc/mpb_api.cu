@@ -20,6 +20,7 @@
 #include "mpb_kernels_split.cuh"
 #include "mpb_sweep.cuh"
 #include "mpb_line.cuh"
+#include "mpb_esprit.cuh"
 
 using namespace mpb;
 
@@ -1788,6 +1789,54 @@ int mpb_comm_info(mpb_handle* h, int32_t* nranks, int32_t* rank, int32_t* nccl_v
 }
 
 int64_t mpb_launch_count(mpb_handle* h) { return h ? h->launches_last : 0; }
+
+int mpb_hankel_mul(int32_t device, const double* x, int64_t n, int32_t columns, int32_t r,
+                   int32_t transpose, const double* in, double* out) {
+    g_err.clear();
+    if (!x || !in || !out || columns < 1 || n < columns || r < 1 || r > kHankelMaxR)
+        return fail_msg(MPB_EINVAL, "hankel: need 1 <= columns <= n and 1 <= r <= %d",
+                        kHankelMaxR);
+    CU(cudaSetDevice(device));
+    const int64_t M = n - columns + 1, L = columns;
+    const int64_t nin = (transpose ? M : L) * r, nout = (transpose ? L : M) * r;
+    double *dx = nullptr, *din = nullptr, *dout = nullptr, *part = nullptr;
+    cudaStream_t s = nullptr;
+    int rc = MPB_OK;
+    auto ok = [&](cudaError_t e, const char* what) {
+        if (e != cudaSuccess && !rc) rc = fail_msg(MPB_ECUDA, "hankel %s: %s", what,
+                                                   cudaGetErrorString(e));
+        return rc == MPB_OK;
+    };
+    if (ok(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream") &&
+        ok(cudaMallocAsync(&dx, sizeof(double) * n, s), "alloc") &&
+        ok(cudaMallocAsync(&din, sizeof(double) * nin, s), "alloc") &&
+        ok(cudaMallocAsync(&dout, sizeof(double) * nout, s), "alloc") &&
+        ok(cudaMemcpyAsync(dx, x, sizeof(double) * n, cudaMemcpyHostToDevice, s), "upload") &&
+        ok(cudaMemcpyAsync(din, in, sizeof(double) * nin, cudaMemcpyHostToDevice, s), "upload")) {
+        if (!transpose) {
+            k_hankel_fwd<<<(unsigned)((M + kHankelTile - 1) / kHankelTile), kHankelTile, 0, s>>>(
+                dx, M, (int)L, r, din, dout);
+        } else {
+            const int split = (int)std::min<int64_t>(kHankelSplit, (M + kHankelTile - 1) / kHankelTile);
+            if (ok(cudaMallocAsync(&part, sizeof(double) * split * nout, s), "alloc")) {
+                k_hankel_tr<<<dim3((unsigned)((L + kHankelTile - 1) / kHankelTile), split),
+                              kHankelTile, 0, s>>>(dx, M, (int)L, r, din, part);
+                k_hankel_sum<<<(unsigned)std::min<int64_t>(1184, (nout + 255) / 256), 256, 0, s>>>(
+                    part, split, nout, dout);
+            }
+        }
+        if (ok(cudaGetLastError(), "launch"))
+            ok(cudaMemcpyAsync(out, dout, sizeof(double) * nout, cudaMemcpyDeviceToHost, s),
+               "download");
+        ok(cudaStreamSynchronize(s), "sync");
+    }
+    if (s) {
+        for (double* p : {dx, din, dout, part}) if (p) cudaFreeAsync(p, s);
+        cudaStreamSynchronize(s);
+        cudaStreamDestroy(s);
+    }
+    return rc;
+}
 
 int64_t mpb_continued_steps(mpb_handle* h) { return h ? h->continued_steps : 0; }
 
