@@ -97,7 +97,14 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
     // of halo plane and pipeline fill)) -- whole waves and long chunks (C4: 8
     // chunks = 7.0 waves, +2% over a fixed 32-wave split; C2 +7%, C3 +3%, C5 +3%)
     const int Fx = g.c1 - g.c0;                      // owned planes of this rank
-    const int per_sm = fs->NT == 256 ? 2 : 1;
+    // fp32 two-CTA form: three CTAs per SM when three rings fit (71
+    // registers; MPB_SWEEP_CTAS=2 keeps two)
+    int per_sm = fs->NT == 256 ? 2 : 1;
+    if (fs->NT == 256 && h->f32 && 3 * (ring_bytes(512) + fixed) <= (size_t)smem_sm) {
+        per_sm = 3;
+        if (const char* e = getenv("MPB_SWEEP_CTAS"))
+            if (atoi(e) == 2) per_sm = 2;
+    }
     const double slots = (double)per_sm * sms;
     int minch = 4;
     if (const char* e = getenv("MPB_SWEEP_MINCHUNK")) minch = std::max(2, atoi(e));
