@@ -569,7 +569,7 @@ k_sweep(Geom g, BufsT<T> b, const mpb_material* __restrict__ mats,
 // local-stop range feed the global stop rule (k_llg_fixup / all-reduce).
 // Ghost-plane copies (slabs) are computed for their H only.
 #ifndef MPB_LLG_MINB
-#define MPB_LLG_MINB 3
+#define MPB_LLG_MINB 2
 #endif
 // One magnetic cell's fixed point to its local stop (CTA statistics in cs).
 template <typename T>
