@@ -100,10 +100,11 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
     // fp32 two-CTA form: three CTAs per SM when three rings fit (71
     // registers; MPB_SWEEP_CTAS=2 keeps two)
     int per_sm = fs->NT == 256 ? 2 : 1;
-    if (fs->NT == 256 && h->f32 && 3 * (ring_bytes(512) + fixed) <= (size_t)smem_sm) {
-        per_sm = 3;
-        if (const char* e = getenv("MPB_SWEEP_CTAS"))
-            if (atoi(e) == 2) per_sm = 2;
+    if (fs->NT == 256 && h->f32) {
+        int want = MPB_F32_CTAS;
+        if (const char* e = getenv("MPB_SWEEP_CTAS")) want = std::max(2, std::min(4, atoi(e)));
+        while (want > 2 && (size_t)want * (ring_bytes(512) + fixed) > (size_t)smem_sm) --want;
+        per_sm = want;
     }
     const double slots = (double)per_sm * sms;
     int minch = 4;

@@ -247,7 +247,10 @@ __device__ __forceinline__ void h_entry(const Geom& g, const HCtx<double>& c, in
 template <int V, bool F3, int NT = kSweepThreads, typename T = double, bool PMC = true>
 // (fp32 two-CTA form: bound for 3 CTAs/SM -- 60 registers, +5% even at 2
 // CTAs/SM; fp64: register caps of 88/80/72 all cost 6-8%)
-__global__ void __launch_bounds__(NT, NT == 256 ? (sizeof(T) == 4 ? 3 : 2) : 1)
+#ifndef MPB_F32_CTAS
+#define MPB_F32_CTAS 3
+#endif
+__global__ void __launch_bounds__(NT, NT == 256 ? (sizeof(T) == 4 ? MPB_F32_CTAS : 2) : 1)
 k_sweep(Geom g, BufsT<T> b, const mpb_material* __restrict__ mats,
         const uint8_t* __restrict__ gids, StepState* st, SweepCfg sc) {
     extern __shared__ __align__(128) unsigned char smem[];
