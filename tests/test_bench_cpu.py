@@ -55,3 +55,27 @@ def test_gpus_flag_must_match_world_size():
                           "--config", "c1"],
                          capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
     assert out.returncode != 0 and "WORLD_SIZE=1" in out.stderr
+
+
+def test_reference_arm_under_torchrun_prints_once():
+    """The driver launches the reference arm like the GPU arm (torchrun, N
+    ranks): rank 0 alone runs and prints one line; the others exit 0."""
+    import os
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                          "--nproc-per-node=2", "--master-addr=127.0.0.1",
+                          f"--master-port={port}", str(ROOT / "bench.py"), "--impl",
+                          "reference", "--gpus", "2", "--steps", "1", "--warmup", "1",
+                          "--config", "c1", "--ref-planes", "4"],
+                         capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    line = json.loads(lines[0])
+    assert line["impl"] == "reference" and line["n_gpus"] == 2
+    assert line["config"]["cells_total"] == 2 * 64 ** 3          # weak scaling: N x C1
