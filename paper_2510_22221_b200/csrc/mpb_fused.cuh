@@ -75,8 +75,6 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
     else        { CU(cudaFuncGetAttributes(&fa, k_sweep<2, true, 256>)); }
     const size_t fixed = fa.sharedSizeBytes + (size_t)reserved;
     const bool f3 = g.act[0] && g.act[1] && g.act[2];
-    // (fp32 storage: 1024-entry tiles in the two-CTA form, V = 4, measured
-    // 1.4% slower on C4 than the same 512-entry tiles; not used)
     if (f3 && g.FyFz >= 2 * 256 * 16 && 2 * (ring_bytes(512) + fixed) <= (size_t)smem_sm) {
         fs->V = 2; fs->NT = 256;
     } else if (g.FyFz >= 2 * kSweepThreads * 64 &&
@@ -85,10 +83,23 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
     } else {
         fs->V = 1; fs->NT = kSweepThreads;
     }
+    bool any_pmc = false;
+    for (int f = 0; f < 6; ++f) any_pmc = any_pmc || g.faces[f] == MPB_FACE_PMC;
+    // fp32 with long z-rows (the halo row > a third of a 512-entry tile,
+    // C5's 257): 1024-entry tiles in the two-CTA form (C5 +2.4%; on C4's
+    // 129-entry rows the 512-entry tiles at three CTAs/SM win by 17%)
+    if (h->f32 && fs->NT == 256 && !any_pmc && 3 * sc.hl > 512 &&
+        2 * (ring_bytes(1024) + fixed) <= (size_t)smem_sm)
+        fs->V = 4;
     if (const char* e = getenv("MPB_SWEEP_V")) {
         const int v = atoi(e);
-        if (v == 1 || v == 2) fs->V = v;
-        if (fs->V != 2) fs->NT = kSweepThreads;
+        if (v == 4 && h->f32 && fs->NT == 256 && !any_pmc &&
+            2 * (ring_bytes(1024) + fixed) <= (size_t)smem_sm) {
+            fs->V = 4;   // fp32: 1024-entry tiles in the two-CTA form
+        } else if (v == 1 || v == 2) {
+            fs->V = v;
+            if (fs->V != 2) fs->NT = kSweepThreads;
+        }
     }
     if (const char* e = getenv("MPB_SWEEP_NT"))
         if (atoi(e) == 512) fs->NT = kSweepThreads;
@@ -103,7 +114,8 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
     if (fs->NT == 256 && h->f32) {
         int want = MPB_F32_CTAS;
         if (const char* e = getenv("MPB_SWEEP_CTAS")) want = std::max(2, std::min(4, atoi(e)));
-        while (want > 2 && (size_t)want * (ring_bytes(512) + fixed) > (size_t)smem_sm) --want;
+        while (want > 2 && (size_t)want * (ring_bytes(fs->V * 256) + fixed) > (size_t)smem_sm)
+            --want;
         per_sm = want;
     }
     const double slots = (double)per_sm * sms;
@@ -195,9 +207,13 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
         if (atoi(e) == 1) fs->pmc = true;
     int rc;
     if (h->f32) {
-        if (fs->NT == 256)
+        if (fs->NT == 256 && fs->V == 4)
+            rc = set_smem_attr<4, true, 256, float, false>(fs->smem);
+        else if (fs->NT == 256)
             rc = fs->pmc ? set_smem_attr<2, true, 256, float>(fs->smem)
                          : set_smem_attr<2, true, 256, float, false>(fs->smem);
+        else if (fs->F3 && fs->V == 2 && !fs->pmc)
+            rc = set_smem_attr<2, true, kSweepThreads, float, false>(fs->smem);
         else if (fs->F3)
             rc = fs->V == 2 ? set_smem_attr<2, true, kSweepThreads, float>(fs->smem)
                             : set_smem_attr<1, true, kSweepThreads, float>(fs->smem);
@@ -207,6 +223,8 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
     } else if (fs->NT == 256) {
         rc = fs->pmc ? set_smem_attr<2, true, 256>(fs->smem)
                      : set_smem_attr<2, true, 256, double, false>(fs->smem);
+    } else if (fs->F3 && fs->V == 2 && !fs->pmc) {   // PMC-free one-CTA form (C5)
+        rc = set_smem_attr<2, true, kSweepThreads, double, false>(fs->smem);
     } else if (fs->F3) {
         rc = fs->V == 2 ? set_smem_attr<2, true>(fs->smem) : set_smem_attr<1, true>(fs->smem);
     } else {
@@ -330,13 +348,22 @@ int launch_fused(mpb_handle* h, const Geom& g, const BufsT<T>& b, cudaStream_t s
     CU(launch_pdl_smem(h->pdl, k_sweep<VV, FF, kSweepThreads, T>, dim3(grid),              \
                        dim3(kSweepThreads), fs->smem, s, g, b, (const mpb_material*)h->mats,  \
                        ids_view(h), h->st, sc))
-    if (fs->NT == 256 && !fs->pmc) {
+    if (fs->NT == 256 && fs->V == 4) {
+        if constexpr (sizeof(T) == 4)   // fp32, PMC-free only (prepare_fused)
+            CU(launch_pdl_smem(h->pdl, k_sweep<4, true, 256, T, false>, dim3(grid), dim3(256),
+                               fs->smem, s, g, b, (const mpb_material*)h->mats, ids_view(h),
+                               h->st, sc));
+    } else if (fs->NT == 256 && !fs->pmc) {
         CU(launch_pdl_smem(h->pdl, k_sweep<2, true, 256, T, false>, dim3(grid), dim3(256),
                            fs->smem, s, g, b, (const mpb_material*)h->mats, ids_view(h), h->st,
                            sc));
     } else if (fs->NT == 256) {
         CU(launch_pdl_smem(h->pdl, k_sweep<2, true, 256, T>, dim3(grid), dim3(256), fs->smem,
                            s, g, b, (const mpb_material*)h->mats, ids_view(h), h->st, sc));
+    } else if (fs->F3 && fs->V == 2 && !fs->pmc) {
+        CU(launch_pdl_smem(h->pdl, k_sweep<2, true, kSweepThreads, T, false>, dim3(grid),
+                           dim3(kSweepThreads), fs->smem, s, g, b, (const mpb_material*)h->mats,
+                           ids_view(h), h->st, sc));
     } else if (fs->F3) {
         if (fs->V == 2) MPB_LAUNCH(2, true);
         else MPB_LAUNCH(1, true);

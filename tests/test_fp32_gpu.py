@@ -74,8 +74,11 @@ def test_fp32_storage_within_tolerance_of_reference(name):
            {k: v.samples for k, v in res.probes.items()}, g["probes"])
 
 
-@pytest.mark.parametrize("name", ["c2", "c3"])
-def test_fp32_benchmark_geometry_within_tolerance(name):
+@pytest.mark.parametrize("name,env", [("c2", None), ("c3", None),
+                                      ("c2", "4")])    # 1024-entry tiles (C5's fp32 form)
+def test_fp32_benchmark_geometry_within_tolerance(name, env, monkeypatch):
+    if env:
+        monkeypatch.setenv("MPB_SWEEP_V", env)
     from tests.test_configs_gpu import mid_run_state
     cfg = load_config(ROOT / "configs" / f"{name}.cfg")
     start, steps = 200, 50
