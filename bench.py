@@ -436,6 +436,8 @@ def main() -> None:
     ap.add_argument("--scaling", default=None, choices=["weak", "strong"],
                     help="multi-GPU mode (default: weak for c1-c4, strong for c5)")
     ap.add_argument("--layout-only", default=None, help=argparse.SUPPRESS)
+    ap.add_argument("--no-secondary", action="store_true",
+                    help="skip the C3 fp64 and C4 fp32 secondary records of the default run")
     args = ap.parse_args()
     if args.scaling is None:
         args.scaling = "strong" if args.config == "c5" else "weak"
@@ -456,14 +458,44 @@ def main() -> None:
 
     import torch
 
-    from paper_2510_22221_b200 import sim
-    from paper_2510_22221_b200.config import load_config
-    from paper_2510_22221_b200.grid import initial_magnetization
-
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    line = measure(args, world, rank, local)
+    if line is None:
+        return
+    if world == 1 and not args.no_secondary and args.config == "c4" and args.dtype == "f64":
+        # secondary records measured by this same run: the LLG-heavy config
+        # (C3: 7% magnetic cells) and the fp32 storage mode on the headline grid
+        line["secondary"] = []
+        for cfg_name, dtype in (("c3", "f64"), ("c4", "f32")):
+            sub = argparse.Namespace(**vars(args))
+            sub.config, sub.dtype, sub.no_cpu = cfg_name, dtype, True
+            sub.scaling = "weak"
+            sub.steps, sub.warmup = max(20, args.steps), max(3, args.warmup)
+            sl = measure(sub, world, rank, local)
+            line["secondary"].append({
+                "workload": sl["config"]["workload"], "dtype": dtype,
+                "value": sl["value"], "unit": sl["unit"], "e2e": sl["e2e"]["value"],
+                "ms_per_step": sl["ms_per_step"], "steps": sl["steps"],
+                "roofline_frac": sl["roofline"]["frac"],
+                "whole_step_frac": sl["roofline"]["whole_step_frac"],
+                "bytes_per_cell": sl["roofline"]["bytes_per_cell"],
+                "magnetic_fraction": sl["config"]["magnetic_fraction"],
+                "clocks": sl["clocks"], "gpu_launches": sl["gpu_launches"]})
+    print(json.dumps(line))
+
+
+def measure(args, world, rank, local):
+    """One bench measurement (timed device region, e2e leg, roofline, CPU
+    baseline unless --no-cpu); returns the JSON line on rank 0, else None."""
+    import torch
+
+    from paper_2510_22221_b200 import sim
+    from paper_2510_22221_b200.config import load_config
+    from paper_2510_22221_b200.grid import initial_magnetization
+
     # painted (lazy) materials: no dense per-cell host maps (C5 would need 69 GB)
     cfg = load_config(ROOT / CONFIGS[args.config], lazy=True)
     cells = int(np.prod(cfg.grid.cell_shape))        # per GPU (weak) / total (strong)
@@ -607,8 +639,8 @@ def main() -> None:
         "gpu_launches": launches,
         "ranks": comm,
     }
-    print(json.dumps(line))
     dev.close()
+    return line
 
 
 if __name__ == "__main__":
