@@ -94,6 +94,12 @@ struct mpb_handle {
     int nmag = 0;                  // local cells (incl. ghost copies)
     int nmag_owned = 0;
     double* scratch = nullptr;
+    // LLG-first step order (MagPre, single rank): compact per-cell H, M
+    // (double-buffered like the lattice) and material ids
+    bool pre = false;
+    void* Hc[2][3] = {};
+    double* Mc[2][3] = {};
+    uint8_t* cid = nullptr;
     StepState* st = nullptr;
     ProbeDesc* probes = nullptr;
     int nprobes = 0;
@@ -168,6 +174,10 @@ int launch_zfix(mpb_handle* h, const Geom& g, const BufsT<T>& b, cudaStream_t s)
 int zfix_launches(mpb_handle* h);
 template <typename T>
 int launch_llg_local(mpb_handle* h, const Geom& g, const BufsT<T>& b, cudaStream_t s);
+template <typename T>
+int launch_llg_pre(mpb_handle* h, int pa, cudaStream_t s);
+template <typename T>
+int pack_magnetic(mpb_handle* h, int pa);
 
 const char* fused_kernel_name();
 void fused_form(mpb_handle* h, int32_t out[4]);
@@ -204,6 +214,23 @@ BufsT<T> make_bufs(const mpb_handle* h, int pa) {
 }
 
 const uint8_t* ids_view(const mpb_handle* h) { return view(h->ids, h); }
+
+template <typename T>
+MagPre<T> make_magpre(const mpb_handle* h, int pa) {
+    MagPre<T> m{};
+    if (!h->pre) return m;
+    const int pb = 1 - pa;
+    for (int c = 0; c < 3; ++c) {
+        m.Hn[c] = static_cast<const T*>(h->Hc[pa][c]);
+        m.Mn[c] = h->Mc[pa][c];
+        m.Hn1[c] = static_cast<T*>(h->Hc[pb][c]);
+        m.Mn1[c] = h->Mc[pb][c];
+        m.Hl[c] = fview<T>(h->H[pa][c], h);
+    }
+    m.cid = h->cid;
+    m.on = 1;
+    return m;
+}
 
 // Stream-ordered allocations on the handle's stream: neither allocating nor
 // freeing a handle synchronises the device, so concurrent runs on one GPU
@@ -362,7 +389,7 @@ int phase_sweep_t(mpb_handle* h, int pa, cudaStream_t s, int64_t& launches, int 
         CU(cudaEventRecord(h->sweep_end, s));
         h->sweep_end = nullptr;
     }
-    if (part != 1 && h->nmag > 0) {
+    if (part != 1 && h->nmag > 0 && !h->pre) {
         if ((rc = launch_llg_local(h, g, b, s))) return rc;
         ++launches;
     }
@@ -414,7 +441,8 @@ int phase_fixup_single_t(mpb_handle* h, int pa, cudaStream_t s, int64_t& launche
     cfg.numAttrs = 1;
     MagScratch scr{h->scratch};
     CU(cudaLaunchKernelEx(&cfg, k_llg_fixup<T>, g, b, (const mpb_material*)h->mats,
-                          ids_view(h), (const int2*)h->magcells, h->nmag, scr, h->st));
+                          ids_view(h), (const int2*)h->magcells, h->nmag, scr, h->st,
+                          make_magpre<T>(h, pa)));
     ++launches;
     return MPB_OK;
 }
@@ -452,7 +480,7 @@ int phase_post_t(mpb_handle* h, int pa, cudaStream_t s, int64_t& launches, bool 
     const Geom& g = h->g;
     const BufsT<T> b = make_bufs<T>(h, pa);
     const uint8_t* ids = ids_view(h);
-    if (h->variant != 1 && h->nmag > 0) {
+    if (h->variant != 1 && h->nmag > 0 && !h->pre) {
         int rc = launch_deferred(h, g, b, s);
         if (rc) return rc;
         ++launches;
@@ -541,6 +569,13 @@ int enqueue_step(mpb_handle* h, int pa, bool timed) {
         CU(cudaEventRecord(e0, s));
         h->sweep_end = e1;
     }
+    if (h->pre) {   // LLG-first: local LLG + r* settlement, then the sweep
+        if ((rc = h->f32 ? launch_llg_pre<float>(h, pa, s) : launch_llg_pre<double>(h, pa, s)))
+            return rc;
+        ++launches;
+        if ((rc = phase_fixup_single(h, pa, s, launches))) return rc;
+        if (timed) CU(cudaEventRecord(e0, s));
+    }
     if ((rc = phase_sweep_overlapped(&h, 1, pa, s, launches))) return rc;
     if (timed) {
         if (h->sweep_end) CU(cudaEventRecord(e1, s));   // split variant: after k_hsweep
@@ -548,7 +583,7 @@ int enqueue_step(mpb_handle* h, int pa, bool timed) {
         h->events.emplace_back(e0, e1);
     }
     if (h->nranks == 1) {
-        if ((rc = phase_fixup_single(h, pa, s, launches))) return rc;
+        if (!h->pre && (rc = phase_fixup_single(h, pa, s, launches))) return rc;
     } else if (h->any_magnetic) {
         // global r*: all-reduce the residual history and local-stop range
         NC(ncclGroupStart());
@@ -957,6 +992,14 @@ int create_body(const mpb_setup* su, mpb_handle* h, int nranks, int x_lo, int x_
     h->rank = nranks == 1 ? 0 : su->rank;
     CU(cudaSetDevice(h->device));
     CU(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    if (const char* e = getenv("MPB_L2FETCH")) {
+        size_t v0 = 0;
+        cudaDeviceGetLimit(&v0, cudaLimitMaxL2FetchGranularity);
+        CU(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(e)));
+        size_t v1 = 0;
+        cudaDeviceGetLimit(&v1, cudaLimitMaxL2FetchGranularity);
+        fprintf(stderr, "mpb: L2 fetch granularity %zu -> %zu\n", v0, v1);
+    }
     if (nranks > 1) {
         CU(cudaStreamCreateWithFlags(&h->comm_stream, cudaStreamNonBlocking));
         CU(cudaEventCreateWithFlags(&h->ev_post, cudaEventDisableTiming));
@@ -1097,10 +1140,6 @@ int create_body(const mpb_setup* su, mpb_handle* h, int nranks, int x_lo, int x_
         CU(cudaFreeAsync(dr, h->stream));
         CU(cudaStreamSynchronize(h->stream));
     }
-    if (h->variant != 1) {
-        rc = prepare_fused(h, g);
-        if (rc) return rc;
-    }
     {   // lines along z that fit in one CTA's shared memory run in k_line
         const char* e = getenv("MPB_LINE");
         const bool want = !(e && atoi(e) == 0);
@@ -1118,6 +1157,30 @@ int create_body(const mpb_setup* su, mpb_handle* h, int nranks, int x_lo, int x_
         }
     }
 
+    // LLG-first step order for single-rank runs of the fused sweep
+    // (MPB_LLG_PRE=0: the LLG after the sweep + deferred E, as multi-rank runs do)
+    {
+        const char* e = getenv("MPB_LLG_PRE");
+        h->pre = !(e && atoi(e) == 0) && nranks == 1 && h->variant == 0 && !h->line &&
+                 h->nmag > 0;
+    }
+    if (h->pre) {
+        for (int p = 0; p < 2; ++p)
+            for (int c = 0; c < 3; ++c) {
+                chk(field_alloc(h, &h->Hc[p][c], (size_t)h->nmag));
+                chk(dev_alloc(h, &h->Mc[p][c], (size_t)h->nmag));
+            }
+        chk(dev_alloc(h, &h->cid, (size_t)h->nmag));
+        if (rc) return rc;
+        std::vector<uint8_t> cid((size_t)h->nmag);
+        for (size_t q = 0; q < cid.size(); ++q)
+            cid[q] = ids[(size_t)((cells[q].x - h->lo) * g.PP + cells[q].y)];
+        CU(cudaMemcpy(h->cid, cid.data(), cid.size(), cudaMemcpyHostToDevice));
+    }
+    if (h->variant != 1) {
+        rc = prepare_fused(h, g);
+        if (rc) return rc;
+    }
     // source (em.py:276-282): only the owning rank injects
     for (int a = 0; a < 3; ++a) {
         if (su->src_loc[a] < 0 || su->src_loc[a] >= g.F[a]) { return fail_msg(MPB_EINVAL, "source location out of range");
@@ -1254,6 +1317,9 @@ void mpb_destroy(mpb_handle* h) {
     dev_free(h, h->magcells);
     dev_free(h, h->magowned);
     dev_free(h, h->scratch);
+    for (int p = 0; p < 2; ++p)
+        for (int c = 0; c < 3; ++c) { dev_free(h, h->Hc[p][c]); dev_free(h, h->Mc[p][c]); }
+    dev_free(h, h->cid);
     dev_free(h, h->st);
     dev_free(h, h->probes);
     dev_free(h, h->d_src);
@@ -1364,6 +1430,8 @@ int mpb_load_state(mpb_handle* h, const double* const fields[6], const double* m
             }
     }
     h->parity = 0;
+    rc = h->f32 ? pack_magnetic<float>(h, 0) : pack_magnetic<double>(h, 0);
+    if (rc) return rc;
     rc = upload_probes(h);
     if (rc) return rc;
     return reset_state(h);

@@ -239,9 +239,20 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
         sc.coef_hf = (float)g.coef_h;
     }
     if (rc) return rc;
+    // LLG-first order: entry range of the magnetic cells within a plane
+    sc.mpre = h->pre ? 1 : 0;
+    sc.mf0 = 0;
+    sc.mf1 = -1;
+    if (h->pre) {
+        std::vector<int2> cells((size_t)h->nmag);
+        CU(cudaMemcpy(cells.data(), h->magcells, sizeof(int2) * cells.size(),
+                      cudaMemcpyDeviceToHost));
+        sc.mf0 = g.FyFz;
+        for (const int2& c : cells) { sc.mf0 = std::min(sc.mf0, c.y); sc.mf1 = std::max(sc.mf1, c.y); }
+    }
     // deferred E entries: {c, c+x, c+y, c+z} over magnetic cells
     std::vector<int64_t> keys;
-    if (h->nmag) {
+    if (h->nmag && !h->pre) {
         std::vector<int2> cells((size_t)h->nmag);
         CU(cudaMemcpy(cells.data(), h->magcells, sizeof(int2) * cells.size(),
                       cudaMemcpyDeviceToHost));
@@ -314,6 +325,28 @@ int launch_llg_local(mpb_handle* h, const Geom& g, const BufsT<T>& b, cudaStream
                        g, b, (const mpb_material*)h->mats, ids_view(h),
                        (const int2*)h->magcells, (const unsigned char*)h->magowned, h->nmag,
                        h->st));
+    return MPB_OK;
+}
+
+// LLG-first order: the magnetic cells' local LLG before the sweep.
+template <typename T>
+int launch_llg_pre(mpb_handle* h, int pa, cudaStream_t s) {
+    const Geom& g = h->g;
+    const size_t smem = (size_t)(g.max_iters + 2) * sizeof(unsigned long long);
+    CU(launch_pdl_smem(h->pdl, k_llg_pre<T>, dim3((h->nmag + 255) / 256), dim3(256), smem, s,
+                       g, make_bufs<T>(h, pa), (const mpb_material*)h->mats,
+                       make_magpre<T>(h, pa), (const int2*)h->magcells, h->nmag, h->st));
+    return MPB_OK;
+}
+
+// compact step-n copy of the magnetic cells from the lattice of parity pa
+template <typename T>
+int pack_magnetic(mpb_handle* h, int pa) {
+    if (!h->pre || !h->nmag) return MPB_OK;
+    k_mag_pack<T><<<(h->nmag + 255) / 256, 256, 0, h->stream>>>(
+        h->g, make_bufs<T>(h, pa), make_magpre<T>(h, pa), (const int2*)h->magcells, h->nmag);
+    CU(cudaGetLastError());
+    CU(cudaStreamSynchronize(h->stream));
     return MPB_OK;
 }
 

@@ -196,7 +196,8 @@ template <typename T>
 __device__ void llg_fixup_grid(const Geom& g, const BufsT<T>& b,
                                const mpb_material* __restrict__ mats,
                                const uint8_t* __restrict__ ids, const int2* __restrict__ cells,
-                               int nmag, MagScratch scr, StepState* st) {
+                               int nmag, MagScratch scr, StepState* st,
+                               const MagPre<T>& mp) {
     __shared__ unsigned long long red[32];
     if (st->fail) return;
     const int rmin = -st->rc_negmin, rmax = st->rc_max;
@@ -226,8 +227,12 @@ __device__ void llg_fixup_grid(const Geom& g, const BufsT<T>& b,
         const int64_t om = (int64_t)(i - g.mx0) * g.PP + f;
         const Curl3 c = curl_e_at(g, b.Ea, o, g.PP, g.F[2], true, true, true);
         double* w = v + (size_t)q * 12;
-        w[0] = b.Ha[0][o]; w[1] = b.Ha[1][o]; w[2] = b.Ha[2][o];
-        w[3] = b.Ma[0][om]; w[4] = b.Ma[1][om]; w[5] = b.Ma[2][om];
+        if (mp.on) {   // LLG-first: the lattice H^n of the cell is overwritten
+            for (int cc = 0; cc < 3; ++cc) { w[cc] = mp.Hn[cc][q]; w[3 + cc] = mp.Mn[cc][q]; }
+        } else {
+            w[0] = b.Ha[0][o]; w[1] = b.Ha[1][o]; w[2] = b.Ha[2][o];
+            w[3] = b.Ma[0][om]; w[4] = b.Ma[1][om]; w[5] = b.Ma[2][om];
+        }
         w[6] = c.x; w[7] = c.y; w[8] = c.z;
         w[9] = w[3]; w[10] = w[4]; w[11] = w[5];
     }
@@ -291,8 +296,15 @@ __device__ void llg_fixup_grid(const Geom& g, const BufsT<T>& b,
         const int64_t om = (int64_t)(i - g.mx0) * g.PP + f;
         const double* w = v + (size_t)q * 12;
         for (int c = 0; c < 3; ++c) {
-            b.Hb[c][o] = (w[c] + (w[3 + c] - w[9 + c])) - g.coef_h * w[6 + c];
+            const double hv = (w[c] + (w[3 + c] - w[9 + c])) - g.coef_h * w[6 + c];
             b.Mb[c][om] = w[9 + c];
+            if (mp.on) {
+                mp.Hl[c][o] = (T)hv;
+                mp.Hn1[c][q] = (T)hv;
+                mp.Mn1[c][q] = w[9 + c];
+            } else {
+                b.Hb[c][o] = hv;
+            }
         }
     }
     if (tid == 0) { st->rstar = rstar; st->fixup_ran = 1; }
@@ -303,10 +315,11 @@ __global__ void __launch_bounds__(256) k_llg_fixup(Geom g, BufsT<T> b,
                                                    const mpb_material* __restrict__ mats,
                                                    const uint8_t* __restrict__ ids,
                                                    const int2* __restrict__ cells, int nmag,
-                                                   MagScratch scr, StepState* st) {
+                                                   MagScratch scr, StepState* st,
+                                                   MagPre<T> mp) {
     pdl_wait();
     pdl_trigger();
-    llg_fixup_grid(g, b, mats, ids, cells, nmag, scr, st);
+    llg_fixup_grid(g, b, mats, ids, cells, nmag, scr, st, mp);
 }
 
 // ---------------------------------------------------------------------------

@@ -143,3 +143,24 @@ def test_gpu_line_general_path_step_failure(monkeypatch):
         sim.run(cfg)
     assert ei.value.step == int(g["fail_step"])
     assert str(ei.value) == str(g["fail_message"])
+
+
+# Single-rank runs compute the magnetic cells' LLG before the sweep (the
+# LLG-first order, k_llg_pre); MPB_LLG_PRE=0 keeps the order multi-rank runs
+# use (sweep, k_llg_local, k_llg_fixup, deferred E).  Both give the same bits.
+@pytest.mark.parametrize("name", RUNNING)
+def test_gpu_llg_after_sweep_order_matches_golden(name, monkeypatch):
+    monkeypatch.setenv("MPB_LLG_PRE", "0")
+    case = CASES[name]
+    _assert_same(sim.run(build(case, mirror_namespace()), bias=case.get("bias")), load(name))
+
+
+@pytest.mark.parametrize("name", ["fail_tol", "fail3d"])
+def test_gpu_llg_after_sweep_order_step_failure(name, monkeypatch):
+    monkeypatch.setenv("MPB_LLG_PRE", "0")
+    g = load(name)
+    with pytest.raises(llg.StepFailure) as ei:
+        sim.run(build(CASES[name], mirror_namespace()))
+    assert ei.value.step == int(g["fail_step"])
+    assert ei.value.iterations == int(g["fail_iterations"])
+    assert ei.value.residual == float(g["fail_residual"])
