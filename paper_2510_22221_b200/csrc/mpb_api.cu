@@ -100,6 +100,7 @@ struct mpb_handle {
     void* Hc[2][3] = {};
     double* Mc[2][3] = {};
     uint8_t* cid = nullptr;
+    std::vector<int2> hcells;      // host copy of magcells (sorted by plane, entry)
     StepState* st = nullptr;
     ProbeDesc* probes = nullptr;
     int nprobes = 0;
@@ -178,6 +179,7 @@ template <typename T>
 int launch_llg_pre(mpb_handle* h, int pa, cudaStream_t s);
 template <typename T>
 int pack_magnetic(mpb_handle* h, int pa);
+int unpack_magnetic(mpb_handle* h);
 
 const char* fused_kernel_name();
 void fused_form(mpb_handle* h, int32_t out[4]);
@@ -920,6 +922,17 @@ int upload_probes(mpb_handle* h) {
         } else if (L[0] >= g.mx0 && L[0] < g.mx1) {
             d.ptr0 = h->M[0][comp - 6]; d.ptr1 = h->M[1][comp - 6];
             d.off = (int64_t)(L[0] - g.mx0) * g.PP + f;
+            if (h->pre) {   // a magnetic cell's M lives in the compact copy
+                const int2 key = make_int2(L[0], (int)f);
+                auto it = std::lower_bound(h->hcells.begin(), h->hcells.end(), key,
+                                           [](const int2& a, const int2& b) {
+                                               return a.x != b.x ? a.x < b.x : a.y < b.y;
+                                           });
+                if (it != h->hcells.end() && it->x == key.x && it->y == key.y) {
+                    d.ptr0 = h->Mc[0][comp - 6]; d.ptr1 = h->Mc[1][comp - 6];
+                    d.off = it - h->hcells.begin();
+                }
+            }
         } else {
             d.ptr0 = d.ptr1 = nullptr;
             d.constant = h->hostM.empty() ? 0.0 :
@@ -992,14 +1005,6 @@ int create_body(const mpb_setup* su, mpb_handle* h, int nranks, int x_lo, int x_
     h->rank = nranks == 1 ? 0 : su->rank;
     CU(cudaSetDevice(h->device));
     CU(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
-    if (const char* e = getenv("MPB_L2FETCH")) {
-        size_t v0 = 0;
-        cudaDeviceGetLimit(&v0, cudaLimitMaxL2FetchGranularity);
-        CU(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(e)));
-        size_t v1 = 0;
-        cudaDeviceGetLimit(&v1, cudaLimitMaxL2FetchGranularity);
-        fprintf(stderr, "mpb: L2 fetch granularity %zu -> %zu\n", v0, v1);
-    }
     if (nranks > 1) {
         CU(cudaStreamCreateWithFlags(&h->comm_stream, cudaStreamNonBlocking));
         CU(cudaEventCreateWithFlags(&h->ev_post, cudaEventDisableTiming));
@@ -1176,6 +1181,7 @@ int create_body(const mpb_setup* su, mpb_handle* h, int nranks, int x_lo, int x_
         for (size_t q = 0; q < cid.size(); ++q)
             cid[q] = ids[(size_t)((cells[q].x - h->lo) * g.PP + cells[q].y)];
         CU(cudaMemcpy(h->cid, cid.data(), cid.size(), cudaMemcpyHostToDevice));
+        h->hcells = cells;
     }
     if (h->variant != 1) {
         rc = prepare_fused(h, g);
@@ -1443,6 +1449,7 @@ int mpb_save_state(mpb_handle* h, double* const fields[6], double* m) {
     const Geom& g = h->g;
     CU(cudaSetDevice(h->device));
     CU(cudaStreamSynchronize(h->stream));
+    if (int rc0 = unpack_magnetic(h)) return rc0;
     const size_t row = (size_t)g.FyFz * sizeof(double);
     const int p = h->parity;
     const int nplanes = h->hi - h->lo;
@@ -1794,6 +1801,7 @@ int mpb_total_energy(mpb_handle* h, double* out) {
     if (!h || !out) return fail_msg(MPB_EINVAL, "null argument");
     CU(cudaSetDevice(h->device));
     CU(cudaStreamSynchronize(h->stream));
+    if (int rc0 = unpack_magnetic(h)) return rc0;
     const Geom& g = h->g;
     const int p = h->parity;
     const void* hp[9];

@@ -350,6 +350,24 @@ int pack_magnetic(mpb_handle* h, int pa) {
     return MPB_OK;
 }
 
+// lattice M of the magnetic cells (current parity) from the compact copy
+int unpack_magnetic(mpb_handle* h) {
+    if (!h->pre || !h->nmag) return MPB_OK;
+    const int p = h->parity;
+    const dim3 grid((h->nmag + 255) / 256);
+    if (h->f32)
+        k_mag_unpack<float><<<grid, 256, 0, h->stream>>>(
+            h->g, h->M[p][0], h->M[p][1], h->M[p][2], make_magpre<float>(h, p),
+            (const int2*)h->magcells, h->nmag);
+    else
+        k_mag_unpack<double><<<grid, 256, 0, h->stream>>>(
+            h->g, h->M[p][0], h->M[p][1], h->M[p][2], make_magpre<double>(h, p),
+            (const int2*)h->magcells, h->nmag);
+    CU(cudaGetLastError());
+    CU(cudaStreamSynchronize(h->stream));
+    return MPB_OK;
+}
+
 void destroy_fused(mpb_handle* h) {
     FusedState* fs = fused_of(h);
     if (!fs) return;

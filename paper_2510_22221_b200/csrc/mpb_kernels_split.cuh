@@ -297,13 +297,13 @@ __device__ void llg_fixup_grid(const Geom& g, const BufsT<T>& b,
         const double* w = v + (size_t)q * 12;
         for (int c = 0; c < 3; ++c) {
             const double hv = (w[c] + (w[3 + c] - w[9 + c])) - g.coef_h * w[6 + c];
-            b.Mb[c][om] = w[9 + c];
             if (mp.on) {
                 mp.Hl[c][o] = (T)hv;
                 mp.Hn1[c][q] = (T)hv;
                 mp.Mn1[c][q] = w[9 + c];
             } else {
                 b.Hb[c][o] = hv;
+                b.Mb[c][om] = w[9 + c];
             }
         }
     }

@@ -654,8 +654,10 @@ __global__ void __launch_bounds__(256, MPB_LLG_MINB) k_llg_local(Geom g, BufsT<T
 
 // LLG-first order (MagPre): one magnetic cell to its local stop from the
 // compact step-n copy; H^{n+1} goes to the compact copy and, in place, to the
-// lattice H^n the sweep stages next; M^{n+1} to the compact copy and the
-// lattice (probes, snapshots, energy).  Single rank: every cell is owned.
+// lattice H^n the sweep stages next; M^{n+1} to the compact copy only (the
+// lattice M of magnetic cells is refreshed from it when a snapshot or the
+// energy reads it; M probes read the compact copy).  Single rank: every cell
+// is owned.
 template <typename T>
 __global__ void __launch_bounds__(256, MPB_LLG_MINB) k_llg_pre(Geom g, BufsT<T> b,
                                                  const mpb_material* __restrict__ mats,
@@ -687,13 +689,11 @@ __global__ void __launch_bounds__(256, MPB_LLG_MINB) k_llg_pre(Geom g, BufsT<T> 
             atomicMax(&cs.hist[r], dbits(res));
             if (res <= g.tol) { rc = r; break; }
         }
-        const int64_t om = (int64_t)(i - g.mx0) * g.PP + f;
         for (int k = 0; k < 3; ++k) {
             const T hv = (T)Hr[k];
             mp.Hl[k][o] = hv;
             mp.Hn1[k][q] = hv;
             mp.Mn1[k][q] = Mr[k];
-            b.Mb[k][om] = Mr[k];
         }
         atomicMin(&cs.rc[0], rc);
         atomicMax(&cs.rc[1], rc);
@@ -716,6 +716,19 @@ __global__ void k_mag_pack(Geom g, BufsT<T> b, MagPre<T> mp, const int2* __restr
         const_cast<T*>(mp.Hn[k])[q] = b.Ha[k][o];
         const_cast<double*>(mp.Mn[k])[q] = b.Ma[k][om];
     }
+}
+
+// lattice M of the magnetic cells from the compact copy (LLG-first order:
+// before a snapshot / energy evaluation reads the lattice)
+template <typename T>
+__global__ void k_mag_unpack(Geom g, double* M0, double* M1, double* M2, MagPre<T> mp,
+                             const int2* __restrict__ cells, int ncells) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= ncells) return;
+    const int64_t om = (int64_t)(cells[q].x - g.mx0) * g.PP + cells[q].y;
+    M0[om] = mp.Mn[0][q];
+    M1[om] = mp.Mn[1][q];
+    M2[om] = mp.Mn[2][q];
 }
 
 // E entries whose curl-H stencil touches a magnetic H entry, recomputed after
