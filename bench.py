@@ -512,7 +512,8 @@ def measure(args, world, rank, local):
     else:
         dev, rank_cells = slab_run(cfg, keys, world, rank, local, args)
     total_cells = cells * world if args.scaling == "weak" else cells
-    total = args.warmup + args.steps
+    gwarm = 32                        # untimed: instantiates the 16-step CUDA graph
+    total = args.warmup + gwarm + 2 * args.steps
     src = torch.tensor(sim.source_values(cfg.source, cfg.dt, 0, total),
                        dtype=torch.float64, device="cuda")
     probe = torch.zeros((total, max(1, len(keys))), dtype=torch.float64, device="cuda")
@@ -523,47 +524,59 @@ def measure(args, world, rank, local):
         if world > 1:
             torch.distributed.barrier()
 
-    # warm-up (W untimed steps)
-    dev.run_device(0, args.warmup, src.data_ptr(), probe.data_ptr(),
-                   iters.data_ptr(), stream.cuda_stream)
+    def run(n0, n):
+        dev.run_device(n0, n, src[n0:].data_ptr(), probe[n0:].data_ptr(), iters[n0:].data_ptr(),
+                       stream.cuda_stream)
+
+    def timed(n0, n):
+        """K steps between a barrier + synchronize on both sides, CUDA events
+        on the launching stream; max over ranks."""
+        barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        run(n0, n)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        t = e0.elapsed_time(e1)
+        if world > 1:
+            tt = torch.tensor([t], dtype=torch.float64, device="cuda")
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            t = float(tt.item())
+        return t
+
+    # warm-up: W untimed steps, then the graph instantiation (untimed)
+    run(0, args.warmup)
+    run(args.warmup, gwarm)
     torch.cuda.synchronize()
     if dev.check_failure() is not None:
         raise RuntimeError("LLG failure during warm-up")
-    # timed region: K steps, device-resident state; dominant kernel timed by
-    # CUDA events on its own stream (library stream) inside the same region
-    dev.set_kernel_timing(True)
+    n0 = args.warmup + gwarm
     clk = ClockSampler(local).start()
-    barrier()
-    torch.cuda.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
     t_wall0 = time.time()
-    e0.record(stream)
-    dev.run_device(args.warmup, args.steps, src[args.warmup:].data_ptr(),
-                   probe[args.warmup:].data_ptr(), iters[args.warmup:].data_ptr(),
-                   stream.cuda_stream)
-    e1.record(stream)
-    torch.cuda.synchronize()
+    # timed region 1 -> value: K steps, device-resident state, the product
+    # path (16-step CUDA graphs)
+    ms = timed(n0, args.steps)
+    launches = dev.launch_count()
+    # timed region 2 -> roofline: the next K steps with CUDA events around
+    # every launch of the dominant kernel on its own (library) stream; the
+    # per-kernel events disable the graphs, so this region's step time is
+    # reported next to the kernel's for the kernel share
+    dev.set_kernel_timing(True)
+    ms_k = timed(n0 + args.steps, args.steps)
     t_wall1 = time.time()
     clk.stop()
-    barrier()
-    ms = e0.elapsed_time(e1)
-    launches = dev.launch_count()
     kms, klaunch, kname = dev.kernel_time()
     dev.set_kernel_timing(False)
     fail = dev.check_failure()
     if fail is not None:
         raise RuntimeError(f"LLG failure in timed region: {fail}")
-    if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
     value = total_cells * args.steps / (ms * 1e-3) / 1e9
     # end-to-end through the C ABI with host buffers (mpb_run)
     e2e_steps = args.e2e_steps or args.steps
-    # untimed warm-up of the host-buffer path: allocates its staging buffers
-    # and instantiates the CUDA graph (the timed run above used per-kernel
-    # events, which disable graphs)
+    # untimed warm-up of the host-buffer path (allocates its staging buffers)
     warm = 32
     _, _, fail = dev.run(total, sim.source_values(cfg.source, cfg.dt, total, total + warm))
     if fail is not None:
@@ -631,7 +644,11 @@ def measure(args, world, rank, local):
                      "traffic": traffic, "kernel": kname,
                      "bytes_per_cell": bpc, "peak_kind": peak_kind,
                      "kernel_ms_per_step": per_launch_ms,
-                     "kernel_share_of_step": per_launch_ms / (ms / args.steps),
+                     "kernel_share_of_step": per_launch_ms / (ms_k / args.steps),
+                     "kernel_timing": "CUDA events around each launch on the library "
+                                      "stream, in a second timed region of K steps "
+                                      f"({ms_k / args.steps:.4f} ms/step there: per-kernel "
+                                      "events disable the CUDA graphs of the first)",
                      "whole_step_frac": step_frac,
                      "whole_step_bytes_per_cell": _bytes_per_cell(f_mag, args.dtype)},
         "cpu_baseline": cpu,
