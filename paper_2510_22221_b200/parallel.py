@@ -207,3 +207,72 @@ def run_group(config, nranks: int, bias=None, device: int = 0, state=None, start
     finally:
         for r in runs:
             r.close()
+
+
+# ---------------------------------------------------------------------------
+# One process per GPU (torchrun): the NCCL data plane
+# ---------------------------------------------------------------------------
+
+def run_ranks(config, bias=None, state=None, start: int = 0):
+    """Run ``config`` as an x-slab decomposition over the ranks of the
+    initialised ``torch.distributed`` process group, one GPU per rank
+    (``LOCAL_RANK``), the halo exchange and LLG all-reduces over NCCL inside
+    the library (mpb_run).  The same contract as :func:`run_group`: on rank 0
+    returns (fields, M, probes, iterations) in the global layout -- equal to
+    sim.run bit for bit -- or (None, None, None, failure); other ranks return
+    None."""
+    import os
+    from dataclasses import replace
+
+    import torch.distributed as dist
+
+    from .grid import initial_magnetization
+    from .sim import _materials_with_bias, source_values
+    world, rank = dist.get_world_size(), dist.get_rank()
+    device = int(os.environ.get("LOCAL_RANK", rank))
+    materials = config.materials if bias is None else _materials_with_bias(
+        config.materials, bias, config.bias_direction)
+    keys = list(dict.fromkeys((p[0], (p[1], p[2], p[3])) for p in config.probes))
+    any_mag = bool(np.count_nonzero(np.asarray(materials.Ms) > 0))
+    nccl_id = nccl_unique_id(dist)
+    sl = replace(make_slabs(config.grid.nx, world, any_mag)[rank], nccl_id=nccl_id)
+    run = slab_device_runs(config, materials, keys, [sl], device=device)[0]
+    try:
+        fs = config.grid.field_shape
+        names = ("Ex", "Ey", "Ez", "Hx", "Hy", "Hz")
+        if state is None:
+            zeros = np.zeros(fs)
+            state = dict({n: zeros for n in names}, M=initial_magnetization(materials))
+        run.load_state({n: local_fields(sl, state[n]) for n in names},
+                       local_cells(sl, state["M"], axis=1))
+        probes, iters, fail = run.run(start, source_values(config.source, config.dt, start,
+                                                           config.n_steps))
+        if fail is not None:
+            part = None
+        else:
+            st = run.save_state()
+            part = {n: owned_part(sl, st[n]) for n in names}
+            part["M"] = owned_cells(sl, st["M"])
+            part["probes"] = probes
+        parts = [None] * world if rank == 0 else None
+        dist.gather_object((sl, part, fail), parts, dst=0)
+    finally:
+        run.close()
+    if rank != 0:
+        return None
+    fails = [f for _, _, f in parts if f is not None]
+    if fails:
+        return None, None, None, fails[0]
+    fields = {n: np.empty(fs) for n in names}
+    M = np.empty((3,) + config.grid.cell_shape)
+    for s, p, _ in parts:
+        c0, c1 = s.owned_fields
+        for n in names:
+            fields[n][c0:c1] = p[n]
+        M[:, s.x_lo:s.x_hi] = p["M"]
+    out_probes = {}
+    for q, (comp, loc) in enumerate(keys):
+        s, p, _ = next(x for x in parts if x[0].owned_fields[0] <= loc[0] < x[0].owned_fields[1])
+        out_probes[(comp, loc)] = p["probes"][:, q].copy()
+    its = np.asarray(iters, dtype=int) if any_mag else np.zeros(0, dtype=int)
+    return fields, M, out_probes, its
