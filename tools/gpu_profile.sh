@@ -4,9 +4,10 @@
 # tools/ncu_summary.py into profiles/).
 set -u
 TAG=${1:-r01}
-CMD="python bench.py --steps 6 --warmup 3 --no-cpu"
+EXTRA=${2:-}
+CMD="python bench.py --steps 6 --warmup 3 --no-cpu --no-secondary $EXTRA"
 mkdir -p gpurun_out
-python bench.py > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_${TAG}.err
+python bench.py $EXTRA > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_${TAG}.err
 tail -1 gpurun_out/bench_${TAG}.json
 $CMD > gpurun_out/plain_${TAG}.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
