@@ -97,6 +97,8 @@ struct mpb_handle {
     // LLG-first step order (MagPre, single rank): compact per-cell H, M
     // (double-buffered like the lattice) and material ids
     bool pre = false;
+    bool pre_coop = false;         // k_llg_pre + fixup as one cooperative launch
+    int coop_blocks = 0;
     void* Hc[2][3] = {};
     double* Mc[2][3] = {};
     uint8_t* cid = nullptr;
@@ -177,6 +179,8 @@ template <typename T>
 int launch_llg_local(mpb_handle* h, const Geom& g, const BufsT<T>& b, cudaStream_t s);
 template <typename T>
 int launch_llg_pre(mpb_handle* h, int pa, cudaStream_t s);
+template <typename T>
+int launch_llg_pre_coop(mpb_handle* h, int pa, cudaStream_t s);
 template <typename T>
 int pack_magnetic(mpb_handle* h, int pa);
 int unpack_magnetic(mpb_handle* h);
@@ -572,10 +576,17 @@ int enqueue_step(mpb_handle* h, int pa, bool timed) {
         h->sweep_end = e1;
     }
     if (h->pre) {   // LLG-first: local LLG + r* settlement, then the sweep
-        if ((rc = h->f32 ? launch_llg_pre<float>(h, pa, s) : launch_llg_pre<double>(h, pa, s)))
-            return rc;
-        ++launches;
-        if ((rc = phase_fixup_single(h, pa, s, launches))) return rc;
+        if (h->pre_coop) {
+            if ((rc = h->f32 ? launch_llg_pre_coop<float>(h, pa, s)
+                             : launch_llg_pre_coop<double>(h, pa, s)))
+                return rc;
+            ++launches;
+        } else {
+            if ((rc = h->f32 ? launch_llg_pre<float>(h, pa, s) : launch_llg_pre<double>(h, pa, s)))
+                return rc;
+            ++launches;
+            if ((rc = phase_fixup_single(h, pa, s, launches))) return rc;
+        }
         if (timed) CU(cudaEventRecord(e0, s));
     }
     if ((rc = phase_sweep_overlapped(&h, 1, pa, s, launches))) return rc;
@@ -1182,6 +1193,23 @@ int create_body(const mpb_setup* su, mpb_handle* h, int nranks, int x_lo, int x_
             cid[q] = ids[(size_t)((cells[q].x - h->lo) * g.PP + cells[q].y)];
         CU(cudaMemcpy(h->cid, cid.data(), cid.size(), cudaMemcpyHostToDevice));
         h->hcells = cells;
+        // one cooperative launch for the local LLG + r* (MPB_LLG_COOP=0: two
+        // launches, k_llg_pre with programmatic launch + k_llg_fixup)
+        h->pre_coop = true;
+        if (const char* e = getenv("MPB_LLG_COOP")) h->pre_coop = atoi(e) != 0;
+        if (h->pre_coop) {
+            const size_t smem = (size_t)(g.max_iters + 2) * sizeof(unsigned long long);
+            int per_sm = 0, sms = 0;
+            if (h->f32) {
+                CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_llg_pre_coop<float>,
+                                                                 256, smem));
+            } else {
+                CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_llg_pre_coop<double>,
+                                                                 256, smem));
+            }
+            CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
+            h->coop_blocks = std::max(1, std::min((h->nmag + 255) / 256, per_sm * sms));
+        }
     }
     if (h->variant != 1) {
         rc = prepare_fused(h, g);

@@ -339,6 +339,25 @@ int launch_llg_pre(mpb_handle* h, int pa, cudaStream_t s) {
     return MPB_OK;
 }
 
+template <typename T>
+int launch_llg_pre_coop(mpb_handle* h, int pa, cudaStream_t s) {
+    const Geom& g = h->g;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(h->coop_blocks);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = (size_t)(g.max_iters + 2) * sizeof(unsigned long long);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CU(cudaLaunchKernelEx(&cfg, k_llg_pre_coop<T>, g, make_bufs<T>(h, pa),
+                          (const mpb_material*)h->mats, make_magpre<T>(h, pa), ids_view(h),
+                          (const int2*)h->magcells, h->nmag, MagScratch{h->scratch}, h->st));
+    return MPB_OK;
+}
+
 // compact step-n copy of the magnetic cells from the lattice of parity pa
 template <typename T>
 int pack_magnetic(mpb_handle* h, int pa) {

@@ -702,6 +702,52 @@ __global__ void __launch_bounds__(256, MPB_LLG_MINB) k_llg_pre(Geom g, BufsT<T> 
     if (lrc[1] > 0) cta_stats_flush(cs, g.max_iters, st);
 }
 
+// The same, fused with the r* settlement: a cooperative grid of co-resident
+// blocks strides over the cells, then one grid barrier and the fixup
+// (uniform replay or lockstep recompute) -- one launch instead of two.
+template <typename T>
+__global__ void __launch_bounds__(256, MPB_LLG_MINB) k_llg_pre_coop(
+    Geom g, BufsT<T> b, const mpb_material* __restrict__ mats, MagPre<T> mp,
+    const uint8_t* __restrict__ ids, const int2* __restrict__ cells, int ncells,
+    MagScratch scr, StepState* st) {
+    extern __shared__ unsigned long long lhist[];
+    __shared__ int lrc[2];
+    if (st->fail) return;
+    CtaLlgStats cs{lhist, lrc};
+    cta_stats_init(cs, g.max_iters);
+    __syncthreads();
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < ncells; q += gridDim.x * blockDim.x) {
+        const int i = cells[q].x, f = cells[q].y;
+        const int64_t o = i * g.PP + f;
+        LlgCell s;
+        for (int k = 0; k < 3; ++k) { s.Hn[k] = (double)mp.Hn[k][q]; s.Mn[k] = mp.Mn[k][q]; }
+        const uint8_t id = mp.cid[q];
+        const Curl3 c = curl_e_at(g, b.Ea, o, g.PP, g.F[2], true, true, true);
+        s.cE[0] = c.x; s.cE[1] = c.y; s.cE[2] = c.z;
+        llg_setup(s, mats[id]);
+        double Hr[3] = {s.Hn[0], s.Hn[1], s.Hn[2]};
+        double Mr[3] = {s.Mn[0], s.Mn[1], s.Mn[2]};
+        int rc = g.max_iters + 1;
+        for (int r = 1; r <= g.max_iters; ++r) {
+            const double res = llg_iterate(s, g.coef_h, Hr, Mr);
+            atomicMax(&cs.hist[r], dbits(res));
+            if (res <= g.tol) { rc = r; break; }
+        }
+        for (int k = 0; k < 3; ++k) {
+            const T hv = (T)Hr[k];
+            mp.Hl[k][o] = hv;
+            mp.Hn1[k][q] = hv;
+            mp.Mn1[k][q] = Mr[k];
+        }
+        atomicMin(&cs.rc[0], rc);
+        atomicMax(&cs.rc[1], rc);
+    }
+    __syncthreads();
+    if (lrc[1] > 0) cta_stats_flush(cs, g.max_iters, st);
+    cg::this_grid().sync();
+    llg_fixup_grid(g, b, mats, ids, cells, ncells, scr, st, mp);
+}
+
 // compact step-n copy of the magnetic cells' H and M from the lattice
 // (after a state load)
 template <typename T>

@@ -164,3 +164,23 @@ def test_gpu_llg_after_sweep_order_step_failure(name, monkeypatch):
     assert ei.value.step == int(g["fail_step"])
     assert ei.value.iterations == int(g["fail_iterations"])
     assert ei.value.residual == float(g["fail_residual"])
+
+
+# LLG-first order as two launches (k_llg_pre with programmatic launch, then
+# the cooperative k_llg_fixup) instead of the default single cooperative one.
+@pytest.mark.parametrize("name", ["mixed3d", "two_magnets", "nonmono3d", "bias3d", "cpw_small"])
+def test_gpu_llg_pre_two_launch_form_matches_golden(name, monkeypatch):
+    monkeypatch.setenv("MPB_LLG_COOP", "0")
+    case = CASES[name]
+    _assert_same(sim.run(build(case, mirror_namespace()), bias=case.get("bias")), load(name))
+
+
+@pytest.mark.parametrize("name", ["fail_tol", "fail3d"])
+def test_gpu_llg_pre_two_launch_form_step_failure(name, monkeypatch):
+    monkeypatch.setenv("MPB_LLG_COOP", "0")
+    g = load(name)
+    with pytest.raises(llg.StepFailure) as ei:
+        sim.run(build(CASES[name], mirror_namespace()))
+    assert ei.value.step == int(g["fail_step"])
+    assert ei.value.iterations == int(g["fail_iterations"])
+    assert ei.value.residual == float(g["fail_residual"])
