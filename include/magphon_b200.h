@@ -167,7 +167,9 @@ MPB_API int mpb_save_state(mpb_handle* h, double* const fields[6], double* m);
  *   probe_out[s*n_probes+p] probe p after step n0+s (sim.py:170-171)
  *   iters_out[s]           LLG iterations r* of step n0+s (sim.py:167)
  * On an LLG failure returns MPB_ESTEP and fills *fail (step = n0+s);
- * probe/iteration rows after the failing step are unspecified. */
+ * probe/iteration rows after the failing step are unspecified, and so is the
+ * device state (the reference raises mid-step too, after its non-magnetic H
+ * update): reload it with mpb_load_state before running again. */
 MPB_API int mpb_run(mpb_handle* h, int64_t n0, int64_t nsteps, const double* src_vals,
             double* probe_out, int32_t* iters_out, mpb_failure* fail);
 
