@@ -455,6 +455,12 @@ def main() -> None:
     if args.layout_only:
         layout_only(args, world, rank)
         return
+    if world > 1:
+        # a rank stuck in a collective (a peer died, a mis-paired exchange)
+        # ends the run with every thread's stack instead of hanging the job
+        import faulthandler
+        faulthandler.dump_traceback_later(int(os.environ.get("MPB_BENCH_WATCHDOG_S", "1200")),
+                                          exit=True)
 
     import torch
 
