@@ -102,7 +102,98 @@ def run_case(name: str, nranks: int) -> str:
             r.close()
 
 
+def _threads(fn, n):
+    errs = []
+
+    def go(q):
+        try:
+            fn(q)
+        except Exception as exc:   # reported by the main thread
+            errs.append(exc)
+
+    ts = [threading.Thread(target=go, args=(q,)) for q in range(n)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    if errs:
+        raise errs[0]
+
+
+def bench_geometry(cfg_name: str, nranks: int, steps: int, dtype: str = "f64") -> str:
+    """bench.py's weak-scaling workload (slab_run: the config's geometry
+    repeated along x, one slab per rank, painted tiled materials, a random
+    mid-run state) through the NCCL branch, against one handle stepping the
+    whole global grid: bit for bit."""
+    from pathlib import Path
+
+    import bench
+    from paper_2510_22221_b200.config import load_config
+    from paper_2510_22221_b200.engine import DeviceRun
+    from paper_2510_22221_b200.grid import GridSpec
+    from paper_2510_22221_b200.sim import _device_run_args
+
+    cfg = load_config(Path(bench.ROOT) / bench.CONFIGS[cfg_name], lazy=True)
+    g = cfg.grid
+    ggrid = GridSpec(g.nx * nranks, g.ny, g.nz, g.dx, g.dy, g.dz)
+    gcfg = replace(cfg, grid=ggrid, probes=())
+    a = _device_run_args(gcfg, [])
+    any_mag = cfg.materials.magnetic_count() > 0
+    gmats = cfg.materials.tiled_region(0, ggrid.nx)
+    state = bench.synthetic_state(ggrid.field_shape, "random")
+    m0 = initial_magnetization(gmats)
+    src = source_values(cfg.source, cfg.dt, 0, steps)
+    kw = {"storage": dtype} if dtype != "f64" else {}
+    # fp32 storage has no bitwise contract across step orders (the sweep forms
+    # E in fp32, the deferred-E kernel in fp64): the single-handle run then
+    # uses the slabs' order (LLG after the sweep); fp64 is the same either way
+    if dtype != "f64":
+        os.environ["MPB_LLG_PRE"] = "0"
+    ref = DeviceRun(ggrid, gmats, a["boundaries"], a["source_loc"], a["source_pol"], [],
+                    cfg.llg_params, cfg.dt, device=0, **kw)
+    os.environ.pop("MPB_LLG_PRE", None)
+    try:
+        ref.load_state(state, m0)
+        _, _, fail = ref.run(0, src)
+        assert fail is None, fail
+        want = ref.save_state()
+    finally:
+        ref.close()
+    nid = nccl_id()
+    slabs = [replace(s, nccl_id=nid) for s in parallel.make_slabs(ggrid.nx, nranks, any_mag)]
+    runs = [DeviceRun(ggrid, cfg.materials.tiled_region(*s.cell_range), a["boundaries"],
+                      a["source_loc"], a["source_pol"], [], cfg.llg_params, cfg.dt, device=0,
+                      slab=s, **kw) for s in slabs]
+    names = ("Ex", "Ey", "Ez", "Hx", "Hy", "Hz")
+    try:
+        for r, sl in zip(runs, slabs):
+            r.load_state({n: parallel.local_fields(sl, state[n]) for n in names},
+                         parallel.local_cells(sl, m0, axis=1))
+        res = [None] * nranks
+
+        def go(q):
+            res[q] = runs[q].run(0, src)
+
+        _threads(go, nranks)
+        assert all(x[2] is None for x in res), [x[2] for x in res]
+        for r, sl in zip(runs, slabs):
+            st = r.save_state()
+            c0, c1 = sl.owned_fields
+            for n in names:
+                assert np.array_equal(parallel.owned_part(sl, st[n]), want[n][c0:c1]), (n, c0)
+            assert np.array_equal(parallel.owned_cells(sl, st["M"]),
+                                  want["M"][:, sl.x_lo:sl.x_hi]), ("M", sl.x_lo)
+    finally:
+        for r in runs:
+            r.close()
+    return f"OK bench {cfg_name} {dtype} x{nranks} {steps} steps"
+
+
 if __name__ == "__main__":
+    if sys.argv[1] == "bench":
+        print(bench_geometry(sys.argv[2], int(sys.argv[3]), int(sys.argv[4]),
+                             sys.argv[5] if len(sys.argv) > 5 else "f64"), flush=True)
+        sys.exit(0)
     n = int(sys.argv[1])
     for name in sys.argv[2:]:
         print(run_case(name, n), flush=True)

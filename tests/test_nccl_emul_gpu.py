@@ -44,3 +44,17 @@ def test_nccl_code_path_matches_reference_goldens(nranks, cases, overlap):
     for name in cases:
         assert any(line.startswith(f"OK {name} x{nranks}") for line in out.stdout.splitlines()), \
             (name, out.stdout)
+
+
+# bench.py's weak-scaling workload itself (slab_run geometry: the config
+# repeated along x, one slab per rank) through the NCCL branch vs one handle
+# stepping the whole global grid
+@pytest.mark.parametrize("cfg,nranks,steps,dtype", [("c2", 2, 6, "f64"), ("c3", 2, 4, "f64"),
+                                                     ("c2", 3, 4, "f32")])
+def test_nccl_code_path_bench_geometry(cfg, nranks, steps, dtype):
+    env = dict(os.environ, LD_PRELOAD=str(_shim()), MPB_SWEEP_MINCHUNK="2")
+    out = subprocess.run([sys.executable, str(ROOT / "tests" / "nccl_emul_worker.py"), "bench",
+                          cfg, str(nranks), str(steps), dtype], cwd=ROOT, env=env,
+                         capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
+    assert f"OK bench {cfg} {dtype} x{nranks}" in out.stdout, out.stdout
