@@ -75,7 +75,7 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
     else        { CU(cudaFuncGetAttributes(&fa, k_sweep<2, true, 256>)); }
     const size_t fixed = fa.sharedSizeBytes + (size_t)reserved;
     const bool f3 = g.act[0] && g.act[1] && g.act[2];
-    if (f3 && g.FyFz >= 2 * 256 * 16 && 2 * (ring_bytes(512) + fixed) <= (size_t)smem_sm) {
+    if (f3 && g.FyFz >= 8 * 512 && 2 * (ring_bytes(512) + fixed) <= (size_t)smem_sm) {
         fs->V = 2; fs->NT = 256;
     } else if (g.FyFz >= 2 * kSweepThreads * 64 &&
                ring_bytes(1024) + fixed <= (size_t)smem_optin) {
@@ -119,7 +119,9 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
         per_sm = want;
     }
     const double slots = (double)per_sm * sms;
-    int minch = 4;
+    // x-chunks of at least 2 planes (C1: 64 planes of 9 tiles need 32 chunks
+    // to fill the 296 CTA slots; the larger grids' choice is unchanged)
+    int minch = 2;
     if (const char* e = getenv("MPB_SWEEP_MINCHUNK")) minch = std::max(2, atoi(e));
     const int maxch = std::max(1, Fx / minch);
     auto chunks_for = [&](int tiles, double* waves_out) {
