@@ -1,4 +1,4 @@
-"""The benchmark geometries (SURVEY 8d C2, C3) on the CUDA path vs the CPU
+"""The benchmark geometries (SURVEY 8d C1, C2, C3) on the CUDA path vs the CPU
 oracle, bit for bit, from a mid-run state.
 
 A fresh run is exact zeros almost everywhere for thousands of steps, so each
@@ -86,7 +86,7 @@ def _check(name, steps):
         assert np.array_equal(res.probes[key].samples, v), key
 
 
-@pytest.mark.parametrize("name,steps", [("c2", 6), ("c3", 4)])
+@pytest.mark.parametrize("name,steps", [("c1", 8), ("c2", 6), ("c3", 4)])
 def test_config_geometry_matches_oracle(name, steps):
     _check(name, steps)
 
@@ -97,6 +97,7 @@ def test_config_geometry_matches_oracle(name, steps):
     {"MPB_SWEEP_NT": "512"},                       # V=2, one 512-thread CTA per SM (C5 form)
     {"MPB_SWEEP_V": "1"},                          # one entry per thread
     {"MPB_SWEEP_T": "334", "MPB_SWEEP_MINCHUNK": "3"},   # ragged tiles and chunks
+    {"MPB_SWEEP_CHUNKS": "128"},                   # two-plane chunks (the C1 choice)
 ])
 def test_sweep_tile_forms_match_oracle(env, monkeypatch):
     for k, v in env.items():
