@@ -140,3 +140,26 @@ def test_simconfig_validation():
         sim.SimConfig(**{**cfg.__dict__, "probes": (("Ex", 0, 0, 10_000),)})
     with pytest.raises(ValueError):
         sim.SimConfig(**{**cfg.__dict__, "t_end": 0.0})
+
+
+def test_nccl_emulation_covers_every_nccl_import(tmp_path):
+    """tests/nccl_emul (the in-process NCCL the multi-rank GPU tests preload)
+    builds for sm_100a and defines every NCCL function the library imports."""
+    import shutil
+    import subprocess
+    if not shutil.which("nvcc") or not shutil.which("nm"):
+        pytest.skip("needs nvcc and nm")
+    lib = _native.LIB_PATH
+    out = tmp_path / "libnccl_emul.so"
+    subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
+                    "-Xcompiler", "-fPIC", "-o", str(out),
+                    str(ROOT / "tests" / "nccl_emul" / "nccl_emul.cu")], check=True)
+
+    def syms(path, kind):
+        text = subprocess.run(["nm", "-D", str(path)], capture_output=True, text=True).stdout
+        return {ln.split()[-1] for ln in text.splitlines()
+                if ln.split()[-2:-1] == [kind] and ln.split()[-1].startswith("nccl")}
+
+    imported = syms(lib, "U")
+    assert "ncclSend" in imported and "ncclAllReduce" in imported
+    assert imported <= syms(out, "T"), imported - syms(out, "T")
