@@ -185,7 +185,8 @@ def _raise_failure(fail, config):
 
 
 def run(config: SimConfig, bias: float | None = None, resume: dict | None = None,
-        *, device: int = 0, kernel_variant: int = 0, storage: str = "f64") -> RunResult:
+        *, device: int = 0, kernel_variant: int = 0, storage: str = "f64",
+        _final_state: bool = True) -> RunResult:
     """Execute a full run on the GPU (reference sim.py:125-180).
 
     With ``bias`` the magnets' bias is overridden along
@@ -235,10 +236,11 @@ def run(config: SimConfig, bias: float | None = None, resume: dict | None = None
         probe_rows, iters, fail = dev.run(start, vals)
         if fail is not None:
             _raise_failure(fail, config)
-        state = dev.save_state()
+        # (a bias sweep keeps only the probes: no final-state download)
+        state = dev.save_state() if _final_state else None
     finally:
         dev.close()
-    lat = FieldLattice.adopt(config.grid, materials, state)
+    lat = FieldLattice.adopt(config.grid, materials, state) if state is not None else None
     b = 0.0 if bias is None else bias
     probes = {}
     for p, key in enumerate(keys):
@@ -301,7 +303,7 @@ class SpectrumMap:
 def _sweep_one(args):
     config, bias, device = args
     from .analysis import fft_magnitude
-    res = run(config, bias=bias, device=device)
+    res = run(config, bias=bias, device=device, _final_state=False)
     probe = list(res.probes.values())[config.spectrum_probe]
     spec = fft_magnitude(probe, window="hann")
     return spec.freqs, spec.mags
