@@ -1310,7 +1310,7 @@ int mpb_create(const mpb_setup* su, mpb_handle** out) {
     if (su->storage == MPB_STORAGE_F32 && su->kernel_variant != 0)
         return fail_msg(MPB_EINVAL, "fp32 storage runs the fused sweep (variant 0) only");
     const int nranks = std::max(1, su->nranks);
-    const int nx = su->n[0], ny = su->n[1], nz = su->n[2];
+    const int nx = su->n[0];
     const int x_lo = nranks == 1 ? 0 : su->x_lo;
     const int x_hi = nranks == 1 ? nx : su->x_hi;
     if (nranks > 1) {
