@@ -75,10 +75,11 @@ def test_fp32_storage_within_tolerance_of_reference(name):
 
 
 @pytest.mark.parametrize("name,env", [("c2", None), ("c3", None),
-                                      ("c2", "4")])    # 1024-entry tiles (C5's fp32 form)
+                                      ("c2", {"MPB_SWEEP_V": "4"}),   # C5's fp32 tile form
+                                      ("c3", {"MPB_LLG_PRE": "0"})])  # LLG after the sweep
 def test_fp32_benchmark_geometry_within_tolerance(name, env, monkeypatch):
-    if env:
-        monkeypatch.setenv("MPB_SWEEP_V", env)
+    for k, v in (env or {}).items():
+        monkeypatch.setenv(k, v)
     from tests.test_configs_gpu import mid_run_state
     cfg = load_config(ROOT / "configs" / f"{name}.cfg")
     start, steps = 200, 50
