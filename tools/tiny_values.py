@@ -12,9 +12,17 @@ from paper_2510_22221_b200.config import load_config  # noqa: E402
 from paper_2510_22221_b200.grid import initial_magnetization  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "c3"
+init = "zero"
+if name.endswith(":random"):
+    name, init = name.split(":")[0], "random"
 cfg = load_config(Path(__file__).resolve().parents[1] / "configs" / f"{name}.cfg", lazy=True)
 dev = sim._device_run(cfg, cfg.materials, [], device=0)
-dev.load_state(None, initial_magnetization(cfg.materials))
+if init == "random":
+    import bench
+    dev.load_state(bench.synthetic_state(cfg.grid.field_shape, "random"),
+                   initial_magnetization(cfg.materials))
+else:
+    dev.load_state(None, initial_magnetization(cfg.materials))
 done = 0
 for n in [int(x) for x in sys.argv[2:]] or [100, 300, 600, 1200]:
     dev.run(done, sim.source_values(cfg.source, cfg.dt, done, n))
