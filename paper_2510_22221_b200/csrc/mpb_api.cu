@@ -326,6 +326,7 @@ int reset_state(mpb_handle* h) {
     memset(&s, 0, sizeof s);
     s.rc_negmin = -0x7fffffff;
     s.fail_step = -1;
+    s.eunsafe_a = 1;      // loaded values unchecked: the first sweep keeps the guard
     CU(cudaMemcpyAsync(h->st, &s, sizeof s, cudaMemcpyHostToDevice, h->stream));
     CU(cudaStreamSynchronize(h->stream));
     return MPB_OK;
@@ -511,7 +512,7 @@ int phase_post_t(mpb_handle* h, int pa, cudaStream_t s, int64_t& launches, bool 
             }
         if (act && !h->wall_per_face) {
             CU(launch_pdl(h->pdl, k_walls_xy<T>, dim3((unsigned)((cnt + 255) / 256), 4), dim3(256),
-                          s, g, b, (const mpb_material*)h->mats, ids, (const StepState*)h->st,
+                          s, g, b, (const mpb_material*)h->mats, ids, h->st,
                           act));
             ++launches;
         }
@@ -1210,6 +1211,14 @@ int create_body(const mpb_setup* su, mpb_handle* h, int nranks, int x_lo, int x_
             CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
             h->coop_blocks = std::max(1, std::min((h->nmag + 255) / 256, per_sm * sms));
         }
+    }
+    // E-range flags (kSafeBias) let the sweep's H phase skip its division
+    // guard; every E writer of this configuration maintains them
+    // (MPB_EGUARD=0: always guarded)
+    {
+        const char* e = getenv("MPB_EGUARD");
+        g.eguard = (!(e && atoi(e) == 0) && nranks == 1 && h->variant == 0 && !h->line &&
+                    !h->f32 && g.zin && !h->wall_per_face && (h->pre || h->nmag == 0)) ? 1 : 0;
     }
     if (h->variant != 1) {
         rc = prepare_fused(h, g);

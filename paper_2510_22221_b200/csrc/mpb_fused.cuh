@@ -241,6 +241,7 @@ int prepare_fused(mpb_handle* h, const Geom& g) {
         sc.coef_hf = (float)g.coef_h;
     }
     if (rc) return rc;
+    sc.eguard = g.eguard;
     // LLG-first order: entry range of the magnetic cells within a plane
     sc.mpre = h->pre ? 1 : 0;
     sc.mf0 = 0;
@@ -312,7 +313,7 @@ int launch_zfix(mpb_handle* h, const Geom& g, const BufsT<T>& b, cudaStream_t s)
     if (!fs->nzlines) return MPB_OK;
     CU(launch_pdl(h->pdl, k_zfix<T>, dim3((fs->nzlines + 255) / 256), dim3(256), s, g, b,
                   (const mpb_material*)h->mats, ids_view(h), (const int3*)fs->zlines,
-                  fs->nzlines, (const StepState*)h->st));
+                  fs->nzlines, h->st));
     return MPB_OK;
 }
 

@@ -597,30 +597,42 @@ __device__ __forceinline__ double wall_value(const Geom& g, const BufsT<T>& b,
 }
 
 // One entry t of x/y wall `face` (active faces: bits of act).
+// Returns max e_range over the valid E entries written (StepState.eunsafe_b).
 template <typename T>
-__device__ __forceinline__ void wall_xy_entry(const Geom& g, const BufsT<T>& b,
-                                              const mpb_material* __restrict__ mats,
-                                              const uint8_t* __restrict__ ids, int act,
-                                              int face, int64_t t) {
+__device__ __forceinline__ unsigned wall_xy_entry(const Geom& g, const BufsT<T>& b,
+                                                  const mpb_material* __restrict__ mats,
+                                                  const uint8_t* __restrict__ ids, int act,
+                                                  int face, int64_t t) {
     const int side = face & 1;
     const int Fz = g.F[2];
+    unsigned eg = 0;
     if (face < 2) {                            // x wall: entries (j, k), Ey and Ez
-        if (t >= (int64_t)g.F[1] * Fz) return;
+        if (t >= (int64_t)g.F[1] * Fz) return 0u;
         const int j = (int)(t / Fz);
+        const int k = (int)(t - (int64_t)j * Fz);
         const int64_t ow = (int64_t)(side ? g.n[0] : 0) * g.PP + t;
         const int64_t oi = (int64_t)(side ? g.n[0] - 1 : 1) * g.PP + t;
-        b.Eb[1][ow] = wall_value(g, b, mats, ids, face, 1, ow, oi);
+        const T vy = wall_value(g, b, mats, ids, face, 1, ow, oi);
+        b.Eb[1][ow] = vy;
+        if (j < g.n[1]) eg = max(eg, e_range((double)vy));
         const bool y_over = (j == 0 && (act & 4)) || (j == g.n[1] && (act & 8));
-        if (!y_over) b.Eb[2][ow] = wall_value(g, b, mats, ids, face, 2, ow, oi);
+        if (!y_over) {
+            const T vz = wall_value(g, b, mats, ids, face, 2, ow, oi);
+            b.Eb[2][ow] = vz;
+            if (k < g.n[2]) eg = max(eg, e_range((double)vz));
+        }
+        return eg;
     } else {                                   // y wall: entries (i, k) of owned planes, Ex and Ez
         const int nown = g.c1 - g.c0;
-        if (t >= (int64_t)nown * Fz) return;
+        if (t >= (int64_t)nown * Fz) return 0u;
         const int i = g.c0 + (int)(t / Fz);
         const int k = (int)(t - (int64_t)(i - g.c0) * Fz);
         const int jw = side ? g.n[1] : 0, jn = side ? g.n[1] - 1 : 1;
         const int64_t ow = (int64_t)i * g.PP + (int64_t)jw * Fz + k;
         const int64_t oi = (int64_t)i * g.PP + (int64_t)jn * Fz + k;
-        b.Eb[0][ow] = wall_value(g, b, mats, ids, face, 0, ow, oi);
+        const T vx = wall_value(g, b, mats, ids, face, 0, ow, oi);
+        b.Eb[0][ow] = vx;
+        if (i < g.n[0]) eg = max(eg, e_range((double)vx));
         // Ez at the inner row, after the x walls
         double ez_in;
         const int xf = (i == 0 && (act & 1)) ? 0 : ((i == g.n[0] && (act & 2)) ? 1 : -1);
@@ -630,12 +642,16 @@ __device__ __forceinline__ void wall_xy_entry(const Geom& g, const BufsT<T>& b,
         } else {
             ez_in = b.Eb[2][oi];
         }
+        T vz;
         if (g.faces[face] == MPB_FACE_PEC) {
-            b.Eb[2][ow] = 0.0;
+            vz = T(0);
         } else {
             const double kk = mats[ids[ow]].mur_k[1];
-            b.Eb[2][ow] = b.Ea[2][oi] + kk * (ez_in - b.Ea[2][ow]);
+            vz = T(b.Ea[2][oi] + kk * (ez_in - b.Ea[2][ow]));
         }
+        b.Eb[2][ow] = vz;
+        if (k < g.n[2]) eg = max(eg, e_range((double)vz));
+        return eg;
     }
 }
 
@@ -643,12 +659,14 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_walls_xy(Geom g, BufsT<T> b,
                                                   const mpb_material* __restrict__ mats,
                                                   const uint8_t* __restrict__ ids,
-                                                  const StepState* st, int act) {
+                                                  StepState* st, int act) {
     pdl_wait();
     pdl_trigger();
     const int face = blockIdx.y;
     if (st->fail || !((act >> face) & 1)) return;
-    wall_xy_entry(g, b, mats, ids, act, face, (int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+    const unsigned eg = wall_xy_entry(g, b, mats, ids, act, face,
+                                      (int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+    if (g.eguard) flag_e_range(eg, &st->eunsafe_b);
 }
 
 // Element-type conversion for fp32-storage uploads/downloads (round to
@@ -721,11 +739,18 @@ __device__ void finish_block(const Geom& g, const BufsT<T>& b, const SourceDesc&
     const long long row = st->local;
     if (threadIdx.x == 0) {
         const double v = st->src_vals[row];
+        unsigned eg = 0;
         for (int c = 0; c < 3; ++c)
             if (src.pol[c] != 0.0) {
                 const double pv = src.pol[c] * v;
                 b.Eb[c][src.off] = (double)b.Eb[c][src.off] + pv;
+                eg = max(eg, e_range((double)b.Eb[c][src.off]));
             }
+        // the E set just completed becomes the next sweep's input
+        if (g.eguard) {
+            st->eunsafe_a = st->eunsafe_b | (eg > kSafeSpan ? 1 : 0);
+            st->eunsafe_b = 0;
+        }
     }
     __syncthreads();
     for (int p = threadIdx.x; p < nprobes; p += blockDim.x) {

@@ -112,6 +112,7 @@ struct SweepCfg {
     float coef_hf;      // fp32 storage mode: dt/mu0 rounded to float
     int mpre;           // LLG-first order: magnetic entries keep their staged H
     int mf0, mf1;       // entry range [mf0, mf1] of the magnetic cells in a plane
+    int eguard;         // E-range flags maintained: the H phase may skip its guard
 };
 
 __global__ void k_recips(double dx, double dy, double dz, double* out) {
@@ -202,6 +203,7 @@ __device__ __forceinline__ void h_entry_f32(const Geom& g, const HCtx<float>& c,
     if (ax) { cy = cy - q4; cz = cz + q5; }
 }
 
+template <bool GUARD = true>
 __device__ __forceinline__ void h_entry(const Geom& g, const HCtx<double>& c, int e, int j, int k,
                                         bool cellplane, int Fz, double ry, double rz,
                                         double rx, double& cx, double& cy, double& cz,
@@ -226,8 +228,9 @@ __device__ __forceinline__ void h_entry(const Geom& g, const HCtx<double>& c, in
     double q3 = qdiv(a3, g.d[2], rz, gY);   // -> cEy
     double q4 = qdiv(a4, g.d[0], rx, gY);   // -> cEy
     double q5 = qdiv(a5, g.d[0], rx, gZ);   // -> cEz
-    const bool bad = !g_fastdiv || (vx && gX > kGuardSpan) || (vy && gY > kGuardSpan) ||
-                     (vz && gZ > kGuardSpan);
+    // (GUARD = false: every E entry is known to be in range, kSafeBias)
+    const bool bad = GUARD && (!g_fastdiv || (vx && gX > kGuardSpan) ||
+                               (vy && gY > kGuardSpan) || (vz && gZ > kGuardSpan));
     if (__builtin_expect(bad, 0)) {
         bool fine = g_fastdiv;
         if (vx) fine = fine && in_range_or_zero(a0) && in_range_or_zero(a2);
@@ -351,6 +354,9 @@ k_sweep(Geom g, BufsT<T> b, const mpb_material* __restrict__ mats,
     const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
     // collapsed axes: their (unused) quotients must not trip the guard
     const bool fastdiv = sc.fastdiv != 0 && ax && ay && az;
+    // the E set this sweep reads is in range: no guard in the H phase
+    const bool hsafe = !kF32 && fastdiv && sc.eguard && st->eunsafe_a == 0;
+    unsigned eg = 0;   // e_range of the valid E values written (next step's flag)
     const bool zw0 = g.zin && az && g.faces[4] != MPB_FACE_PMC;
     const bool zw1 = g.zin && az && g.faces[5] != MPB_FACE_PMC;
     const bool z0pec = g.faces[4] == MPB_FACE_PEC, z1pec = g.faces[5] == MPB_FACE_PEC;
@@ -404,7 +410,7 @@ k_sweep(Geom g, BufsT<T> b, const mpb_material* __restrict__ mats,
         // two copies of the loop: the test sits only in the one run by the
         // planes / tiles that hold magnetic cells (in the common loop even a
         // predicated test cost the C4 sweep 2.5%)
-        auto h_phase = [&](auto PM) {
+        auto h_phase = [&](auto PM, auto SAFE) {
             for (int gg = hlo + tid; gg < f1; gg += NT) {
                 const int j = fz_div((uint32_t)gg, sc.fz_magic);
                 const int k = gg - j * Fz;
@@ -425,8 +431,9 @@ k_sweep(Geom g, BufsT<T> b, const mpb_material* __restrict__ mats,
                     if (vz) hc.Hz[e] = hc.Hz[e] - sc.coef_hf * cz;
                 } else {
                     double cx, cy, cz;
-                    h_entry(g, hc, e, j, k, cellplane, Fz, ry, rz, rx, cx, cy, cz, vx, vy, vz,
-                            fastdiv, ax, ay, az);
+                    h_entry<!decltype(SAFE)::value>(g, hc, e, j, k, cellplane, Fz, ry, rz, rx,
+                                                      cx, cy, cz, vx, vy, vz, fastdiv, ax, ay,
+                                                      az);
                     vx = vx && !keep; vy = vy && !keep; vz = vz && !keep;
                     if (vx) hc.Hx[e] = hc.Hx[e] - g.coef_h * cx;
                     if (vy) hc.Hy[e] = hc.Hy[e] - g.coef_h * cy;
@@ -434,8 +441,13 @@ k_sweep(Geom g, BufsT<T> b, const mpb_material* __restrict__ mats,
                 }
             }
         };
-        if (pm) h_phase(std::true_type{});
-        else h_phase(std::false_type{});
+        if (hsafe) {
+            if (pm) h_phase(std::true_type{}, std::true_type{});
+            else h_phase(std::false_type{}, std::true_type{});
+        } else {
+            if (pm) h_phase(std::true_type{}, std::false_type{});
+            else h_phase(std::false_type{}, std::false_type{});
+        }
         // H^{n+1}(p) complete everywhere, and every thread is past E(p-1) and
         // H(p), the last readers of plane p-1's slot: refill it with p+2
         __syncthreads();
@@ -552,15 +564,33 @@ k_sweep(Geom g, BufsT<T> b, const mpb_material* __restrict__ mats,
                     if (wx) b.Eb[0][o] = w0;
                     if (wy) b.Eb[1][o] = w1;
                     b.Eb[2][o] = w2;
+                    // valid entries: Ex on cell planes, Ey below row ny, Ez below nz
+                    if constexpr (!kF32) {
+                        if (wx && cellplane) eg = max(eg, e_range(w0));
+                        if (wy && jlt) eg = max(eg, e_range(w1));
+                        if (klt) eg = max(eg, e_range(w2));
+                    }
                     if (zw0 && k1) {
                         const T kk = s_murz[ids[f - 1 - ia0]];
-                        if (zx) b.Eb[0][o - 1] = z0pec ? zero : exa + kk * (w0 - Ex[e - 1]);
-                        if (zy) b.Eb[1][o - 1] = z0pec ? zero : eya + kk * (w1 - Ey[e - 1]);
+                        const T v0 = z0pec ? zero : exa + kk * (w0 - Ex[e - 1]);
+                        const T v1 = z0pec ? zero : eya + kk * (w1 - Ey[e - 1]);
+                        if (zx) b.Eb[0][o - 1] = v0;
+                        if (zy) b.Eb[1][o - 1] = v1;
+                        if constexpr (!kF32) {
+                            if (zx && cellplane) eg = max(eg, e_range(v0));
+                            if (zy && jlt) eg = max(eg, e_range(v1));
+                        }
                     }
                     if (zw1 && kn1) {
                         const T kk = s_murz[ids[f + 1 - ia0]];
-                        if (zx) b.Eb[0][o + 1] = z1pec ? zero : exa + kk * (w0 - Ex[e + 1]);
-                        if (zy) b.Eb[1][o + 1] = z1pec ? zero : eya + kk * (w1 - Ey[e + 1]);
+                        const T v0 = z1pec ? zero : exa + kk * (w0 - Ex[e + 1]);
+                        const T v1 = z1pec ? zero : eya + kk * (w1 - Ey[e + 1]);
+                        if (zx) b.Eb[0][o + 1] = v0;
+                        if (zy) b.Eb[1][o + 1] = v1;
+                        if constexpr (!kF32) {
+                            if (zx && cellplane) eg = max(eg, e_range(v0));
+                            if (zy && jlt) eg = max(eg, e_range(v1));
+                        }
                     }
                     if constexpr (!kBulkH) {
                         const bool cp = p < nx || !ax;
@@ -582,6 +612,8 @@ k_sweep(Geom g, BufsT<T> b, const mpb_material* __restrict__ mats,
             }
         }
     }
+    if constexpr (!kF32)
+        if (sc.eguard) flag_e_range(eg, &st->eunsafe_b);
     if (kBulkH && tid == kIssuer) bulk_wait_all();   // slots live until the stores read them
 }
 
@@ -835,23 +867,32 @@ __global__ void __launch_bounds__(256) k_edefer(Geom g, BufsT<T> b,
 // list entries: (comp, i, j) packed as int3.
 // One z-wall fix-up line entry (see k_zfix).
 template <typename T>
-__device__ __forceinline__ void zfix_line(const Geom& g, const BufsT<T>& b,
-                                          const mpb_material* __restrict__ mats,
-                                          const uint8_t* __restrict__ ids,
-                                          const int3* __restrict__ lines, int q) {
+__device__ __forceinline__ unsigned zfix_line(const Geom& g, const BufsT<T>& b,
+                                              const mpb_material* __restrict__ mats,
+                                              const uint8_t* __restrict__ ids,
+                                              const int3* __restrict__ lines, int q) {
     const int c = lines[q].x, i = lines[q].y, j = lines[q].z;
     const int64_t row = i * g.PP + (int64_t)j * g.F[2];
     const int nz = g.n[2];
+    const bool valid = c == 0 ? i < g.n[0] : j < g.n[1];   // Ex / Ey entry exists
+    unsigned eg = 0;
     if (g.faces[4] != MPB_FACE_PMC) {     // z0: wall 0, inner 1
         const int64_t ow = row, oi = row + 1;
-        if (g.faces[4] == MPB_FACE_PEC) b.Eb[c][ow] = 0.0;
-        else b.Eb[c][ow] = b.Ea[c][oi] + mats[ids[ow]].mur_k[2] * (b.Eb[c][oi] - b.Ea[c][ow]);
+        const T v = g.faces[4] == MPB_FACE_PEC
+                        ? T(0)
+                        : T(b.Ea[c][oi] + mats[ids[ow]].mur_k[2] * (b.Eb[c][oi] - b.Ea[c][ow]));
+        b.Eb[c][ow] = v;
+        if (valid) eg = max(eg, e_range((double)v));
     }
     if (g.faces[5] != MPB_FACE_PMC) {     // z1: wall nz, inner nz-1
         const int64_t ow = row + nz, oi = row + nz - 1;
-        if (g.faces[5] == MPB_FACE_PEC) b.Eb[c][ow] = 0.0;
-        else b.Eb[c][ow] = b.Ea[c][oi] + mats[ids[ow]].mur_k[2] * (b.Eb[c][oi] - b.Ea[c][ow]);
+        const T v = g.faces[5] == MPB_FACE_PEC
+                        ? T(0)
+                        : T(b.Ea[c][oi] + mats[ids[ow]].mur_k[2] * (b.Eb[c][oi] - b.Ea[c][ow]));
+        b.Eb[c][ow] = v;
+        if (valid) eg = max(eg, e_range((double)v));
     }
+    return eg;
 }
 
 template <typename T>
@@ -859,12 +900,13 @@ __global__ void __launch_bounds__(256) k_zfix(Geom g, BufsT<T> b,
                                               const mpb_material* __restrict__ mats,
                                               const uint8_t* __restrict__ ids,
                                               const int3* __restrict__ lines, int n,
-                                              const StepState* st) {
+                                              StepState* st) {
     pdl_wait();
     pdl_trigger();
     if (st->fail) return;
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (q < n) zfix_line(g, b, mats, ids, lines, q);
+    const unsigned eg = q < n ? zfix_line(g, b, mats, ids, lines, q) : 0u;
+    if (g.eguard) flag_e_range(eg, &st->eunsafe_b);
 }
 
 }  // namespace mpb
