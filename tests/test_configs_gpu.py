@@ -125,3 +125,19 @@ def test_nonzero_m_outside_magnets_is_preserved():
         assert np.array_equal(res.lattice.state_arrays()[k], v), k
     for key, v in ref["probes"].items():
         assert np.array_equal(res.probes[key].samples, v), key
+
+
+def test_guard_free_h_phase_is_bitwise_through_a_run_from_rest(monkeypatch):
+    """The sweep's H phase skips the exact-division guard only while a
+    per-step flag proves every E value in range (kSafeBias); a run from rest
+    goes through zeros and a shell of tiny values ahead of its wavefront, so
+    the flag switches both ways.  Same bits as with the guard always on."""
+    cfg = load_config(ROOT / "configs" / "c3.cfg")
+    cfg = replace(cfg, t_end=(400 - 0.5) * cfg.dt)
+    a = sim.run(cfg)
+    monkeypatch.setenv("MPB_EGUARD", "0")
+    b = sim.run(cfg)
+    for k, v in b.lattice.state_arrays().items():
+        assert np.array_equal(a.lattice.state_arrays()[k], v), k
+    for key, v in b.probes.items():
+        assert np.array_equal(a.probes[key].samples, v.samples), key
