@@ -585,26 +585,20 @@ __global__ void __launch_bounds__(256) k_wall(Geom g, BufsT<T> b,
 // it).  Every other read is of entries no wall writes.  act: bit f = face f
 // active on this rank.
 // ---------------------------------------------------------------------------
-template <typename T>
-__device__ __forceinline__ double wall_value(const Geom& g, const BufsT<T>& b,
-                                             const mpb_material* __restrict__ mats,
-                                             const uint8_t* __restrict__ ids, int face, int c,
-                                             int64_t ow, int64_t oi) {
-    if (g.faces[face] == MPB_FACE_PEC) return 0.0;
-    // MUR1: wall = prev_inner + k (inner_new - prev_wall)
-    const double kk = mats[ids[ow]].mur_k[face >> 1];
-    return b.Ea[c][oi] + kk * (b.Eb[c][oi] - b.Ea[c][ow]);
-}
-
 // One entry t of x/y wall `face` (active faces: bits of act).
 // Returns max e_range over the valid E entries written (StepState.eunsafe_b).
+// Every load of the entry is issued before the first store and alongside the
+// kernel's fail flag (the stores go to other arrays than the loads read, which
+// the compiler cannot prove): two round trips (E + ids, then the material's
+// MUR coefficient) instead of a chain of five.
 template <typename T>
 __device__ __forceinline__ unsigned wall_xy_entry(const Geom& g, const BufsT<T>& b,
                                                   const mpb_material* __restrict__ mats,
                                                   const uint8_t* __restrict__ ids, int act,
-                                                  int face, int64_t t) {
+                                                  int face, int64_t t, int fail) {
     const int side = face & 1;
     const int Fz = g.F[2];
+    const bool mur = g.faces[face] != MPB_FACE_PEC;
     unsigned eg = 0;
     if (face < 2) {                            // x wall: entries (j, k), Ey and Ez
         if (t >= (int64_t)g.F[1] * Fz) return 0u;
@@ -612,12 +606,22 @@ __device__ __forceinline__ unsigned wall_xy_entry(const Geom& g, const BufsT<T>&
         const int k = (int)(t - (int64_t)j * Fz);
         const int64_t ow = (int64_t)(side ? g.n[0] : 0) * g.PP + t;
         const int64_t oi = (int64_t)(side ? g.n[0] - 1 : 1) * g.PP + t;
-        const T vy = wall_value(g, b, mats, ids, face, 1, ow, oi);
+        const bool y_over = (j == 0 && (act & 4)) || (j == g.n[1] && (act & 8));
+        double a1i = 0, b1i = 0, a1w = 0, a2i = 0, b2i = 0, a2w = 0;
+        uint8_t id = 0;
+        if (mur) {
+            id = ids[ow];
+            a1i = b.Ea[1][oi]; b1i = b.Eb[1][oi]; a1w = b.Ea[1][ow];
+            if (!y_over) { a2i = b.Ea[2][oi]; b2i = b.Eb[2][oi]; a2w = b.Ea[2][ow]; }
+        }
+        if (fail) return 0u;
+        const double kk = mur ? mats[id].mur_k[0] : 0.0;
+        // MUR1: wall = prev_inner + k (inner_new - prev_wall)
+        const T vy = mur ? T(a1i + kk * (b1i - a1w)) : T(0);
         b.Eb[1][ow] = vy;
         if (j < g.n[1]) eg = max(eg, e_range((double)vy));
-        const bool y_over = (j == 0 && (act & 4)) || (j == g.n[1] && (act & 8));
         if (!y_over) {
-            const T vz = wall_value(g, b, mats, ids, face, 2, ow, oi);
+            const T vz = mur ? T(a2i + kk * (b2i - a2w)) : T(0);
             b.Eb[2][ow] = vz;
             if (k < g.n[2]) eg = max(eg, e_range((double)vz));
         }
@@ -630,24 +634,35 @@ __device__ __forceinline__ unsigned wall_xy_entry(const Geom& g, const BufsT<T>&
         const int jw = side ? g.n[1] : 0, jn = side ? g.n[1] - 1 : 1;
         const int64_t ow = (int64_t)i * g.PP + (int64_t)jw * Fz + k;
         const int64_t oi = (int64_t)i * g.PP + (int64_t)jn * Fz + k;
-        const T vx = wall_value(g, b, mats, ids, face, 0, ow, oi);
+        // Ez at the inner row, after the x walls (recomputed: the x faces run
+        // in the same launch)
+        const int xf = (i == 0 && (act & 1)) ? 0 : ((i == g.n[0] && (act & 2)) ? 1 : -1);
+        const bool xmur = xf >= 0 && g.faces[xf] != MPB_FACE_PEC;
+        double a0i = 0, b0i = 0, a0w = 0, a2i = 0, a2w = 0, b2i = 0, b2x = 0, a2x = 0;
+        uint8_t id = 0, idx = 0;
+        if (mur) {
+            id = ids[ow];
+            a0i = b.Ea[0][oi]; b0i = b.Eb[0][oi]; a0w = b.Ea[0][ow];
+            a2i = b.Ea[2][oi]; a2w = b.Ea[2][ow];
+            if (xf < 0) b2i = b.Eb[2][oi];
+        }
+        if (mur && xmur) {
+            const int64_t xin = (int64_t)(xf ? g.n[0] - 1 : 1) * g.PP + (int64_t)jn * Fz + k;
+            idx = ids[oi]; b2x = b.Eb[2][xin]; a2x = b.Ea[2][xin];
+        }
+        if (fail) return 0u;
+        const double kk = mur ? mats[id].mur_k[1] : 0.0;
+        const T vx = mur ? T(a0i + kk * (b0i - a0w)) : T(0);
         b.Eb[0][ow] = vx;
         if (i < g.n[0]) eg = max(eg, e_range((double)vx));
-        // Ez at the inner row, after the x walls
-        double ez_in;
-        const int xf = (i == 0 && (act & 1)) ? 0 : ((i == g.n[0] && (act & 2)) ? 1 : -1);
-        if (xf >= 0) {
-            const int64_t xin = (int64_t)(xf ? g.n[0] - 1 : 1) * g.PP + (int64_t)jn * Fz + k;
-            ez_in = wall_value(g, b, mats, ids, xf, 2, oi, xin);
-        } else {
-            ez_in = b.Eb[2][oi];
-        }
         T vz;
-        if (g.faces[face] == MPB_FACE_PEC) {
+        if (!mur) {
             vz = T(0);
         } else {
-            const double kk = mats[ids[ow]].mur_k[1];
-            vz = T(b.Ea[2][oi] + kk * (ez_in - b.Ea[2][ow]));
+            double ez_in;
+            if (xf >= 0) ez_in = xmur ? a2x + mats[idx].mur_k[0] * (b2x - a2i) : 0.0;
+            else ez_in = b2i;
+            vz = T(a2i + kk * (ez_in - a2w));
         }
         b.Eb[2][ow] = vz;
         if (k < g.n[2]) eg = max(eg, e_range((double)vz));
@@ -663,9 +678,11 @@ __global__ void __launch_bounds__(256) k_walls_xy(Geom g, BufsT<T> b,
     pdl_wait();
     pdl_trigger();
     const int face = blockIdx.y;
-    if (st->fail || !((act >> face) & 1)) return;
+    if (!((act >> face) & 1)) return;
+    const int fail = st->fail;   // in flight with the entry's loads
     const unsigned eg = wall_xy_entry(g, b, mats, ids, act, face,
-                                      (int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+                                      (int64_t)blockIdx.x * blockDim.x + threadIdx.x, fail);
+    if (fail) return;
     if (g.eguard) flag_e_range(eg, &st->eunsafe_b);
 }
 
@@ -735,32 +752,55 @@ template <typename T>
 __device__ void finish_block(const Geom& g, const BufsT<T>& b, const SourceDesc& src,
                              const ProbeDesc* __restrict__ probes, int nprobes, int parity_b,
                              int record_iters, StepState* st) {
-    if (st->fail) return;
+    // A chain of dependent round trips is this kernel's whole cost, so every
+    // load that does not depend on another is issued up front: the fail flag,
+    // the row, the source entries and each thread's first probe value (a
+    // probe on the source entry is re-read after the injection).
+    const int fail = st->fail;
     const long long row = st->local;
+    double e0[3] = {0.0, 0.0, 0.0};
+    unsigned eub = 0;
+    if (threadIdx.x == 0) {
+        for (int c = 0; c < 3; ++c)
+            if (src.pol[c] != 0.0) e0[c] = (double)b.Eb[c][src.off];
+        if (g.eguard) eub = st->eunsafe_b;
+    }
+    auto probe_value = [&](const ProbeDesc& pd) -> double {
+        const void* base = parity_b ? pd.ptr1 : pd.ptr0;
+        return !base ? pd.constant
+                     : (pd.f32 ? (double)static_cast<const float*>(base)[pd.off]
+                               : static_cast<const double*>(base)[pd.off]);
+    };
+    double pv0 = 0.0;
+    ProbeDesc pd0{};
+    if ((int)threadIdx.x < nprobes) {
+        pd0 = probes[threadIdx.x];
+        pv0 = probe_value(pd0);
+    }
+    if (fail) return;
     if (threadIdx.x == 0) {
         const double v = st->src_vals[row];
         unsigned eg = 0;
         for (int c = 0; c < 3; ++c)
             if (src.pol[c] != 0.0) {
                 const double pv = src.pol[c] * v;
-                b.Eb[c][src.off] = (double)b.Eb[c][src.off] + pv;
-                eg = max(eg, e_range((double)b.Eb[c][src.off]));
+                const T nv = e0[c] + pv;
+                b.Eb[c][src.off] = nv;
+                eg = max(eg, e_range((double)nv));
             }
         // the E set just completed becomes the next sweep's input
         if (g.eguard) {
-            st->eunsafe_a = st->eunsafe_b | (eg > kSafeSpan ? 1 : 0);
+            st->eunsafe_a = eub | (eg > kSafeSpan ? 1 : 0);
             st->eunsafe_b = 0;
         }
     }
     __syncthreads();
-    for (int p = threadIdx.x; p < nprobes; p += blockDim.x) {
-        const ProbeDesc pd = probes[p];
-        const void* base = parity_b ? pd.ptr1 : pd.ptr0;
-        st->probe_out[row * nprobes + p] =
-            !base ? pd.constant
-                  : (pd.f32 ? (double)static_cast<const float*>(base)[pd.off]
-                            : static_cast<const double*>(base)[pd.off]);
+    if ((int)threadIdx.x < nprobes) {
+        if (pd0.off == src.off) pv0 = probe_value(pd0);   // may sample the injected entry
+        st->probe_out[row * nprobes + threadIdx.x] = pv0;
     }
+    for (int p = threadIdx.x + blockDim.x; p < nprobes; p += blockDim.x)
+        st->probe_out[row * nprobes + p] = probe_value(probes[p]);
     for (int r = threadIdx.x; r <= g.max_iters + 1; r += blockDim.x) {
         st->hist[r] = 0ull;
         st->hist2[r] = 0ull;

@@ -870,26 +870,31 @@ template <typename T>
 __device__ __forceinline__ unsigned zfix_line(const Geom& g, const BufsT<T>& b,
                                               const mpb_material* __restrict__ mats,
                                               const uint8_t* __restrict__ ids,
-                                              const int3* __restrict__ lines, int q) {
+                                              const int3* __restrict__ lines, int q,
+                                              int fail) {
     const int c = lines[q].x, i = lines[q].y, j = lines[q].z;
     const int64_t row = i * g.PP + (int64_t)j * g.F[2];
     const int nz = g.n[2];
     const bool valid = c == 0 ? i < g.n[0] : j < g.n[1];   // Ex / Ey entry exists
+    // both faces' loads before either store (one round trip, not two); with
+    // nz == 1 the z1 inner entry is the z0 wall just written: re-read it
+    const bool m0 = g.faces[4] == MPB_FACE_MUR1, m1 = g.faces[5] == MPB_FACE_MUR1;
+    const int64_t ow0 = row, oi0 = row + 1, ow1 = row + nz, oi1 = row + nz - 1;
+    double a0i = 0, b0i = 0, a0w = 0, a1i = 0, b1i = 0, a1w = 0;
+    uint8_t id0 = 0, id1 = 0;
+    if (m0) { a0i = b.Ea[c][oi0]; b0i = b.Eb[c][oi0]; a0w = b.Ea[c][ow0]; id0 = ids[ow0]; }
+    if (m1) { a1i = b.Ea[c][oi1]; b1i = b.Eb[c][oi1]; a1w = b.Ea[c][ow1]; id1 = ids[ow1]; }
+    if (fail) return 0u;
     unsigned eg = 0;
     if (g.faces[4] != MPB_FACE_PMC) {     // z0: wall 0, inner 1
-        const int64_t ow = row, oi = row + 1;
-        const T v = g.faces[4] == MPB_FACE_PEC
-                        ? T(0)
-                        : T(b.Ea[c][oi] + mats[ids[ow]].mur_k[2] * (b.Eb[c][oi] - b.Ea[c][ow]));
-        b.Eb[c][ow] = v;
+        const T v = !m0 ? T(0) : T(a0i + mats[id0].mur_k[2] * (b0i - a0w));
+        b.Eb[c][ow0] = v;
         if (valid) eg = max(eg, e_range((double)v));
     }
     if (g.faces[5] != MPB_FACE_PMC) {     // z1: wall nz, inner nz-1
-        const int64_t ow = row + nz, oi = row + nz - 1;
-        const T v = g.faces[5] == MPB_FACE_PEC
-                        ? T(0)
-                        : T(b.Ea[c][oi] + mats[ids[ow]].mur_k[2] * (b.Eb[c][oi] - b.Ea[c][ow]));
-        b.Eb[c][ow] = v;
+        if (m1 && oi1 == ow0) b1i = b.Eb[c][oi1];
+        const T v = !m1 ? T(0) : T(a1i + mats[id1].mur_k[2] * (b1i - a1w));
+        b.Eb[c][ow1] = v;
         if (valid) eg = max(eg, e_range((double)v));
     }
     return eg;
@@ -903,9 +908,10 @@ __global__ void __launch_bounds__(256) k_zfix(Geom g, BufsT<T> b,
                                               StepState* st) {
     pdl_wait();
     pdl_trigger();
-    if (st->fail) return;
+    const int fail = st->fail;   // in flight with the line's loads
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
-    const unsigned eg = q < n ? zfix_line(g, b, mats, ids, lines, q) : 0u;
+    const unsigned eg = q < n ? zfix_line(g, b, mats, ids, lines, q, fail) : 0u;
+    if (fail) return;
     if (g.eguard) flag_e_range(eg, &st->eunsafe_b);
 }
 
