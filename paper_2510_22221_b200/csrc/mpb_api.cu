@@ -327,6 +327,7 @@ int reset_state(mpb_handle* h) {
     s.rc_negmin = -0x7fffffff;
     s.fail_step = -1;
     s.eunsafe_a = 1;      // loaded values unchecked: the first sweep keeps the guard
+    s.llg_stamp = -1;
     CU(cudaMemcpyAsync(h->st, &s, sizeof s, cudaMemcpyHostToDevice, h->stream));
     CU(cudaStreamSynchronize(h->stream));
     return MPB_OK;
@@ -1210,6 +1211,10 @@ int create_body(const mpb_setup* su, mpb_handle* h, int nranks, int x_lo, int x_
             }
             CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
             h->coop_blocks = std::max(1, std::min((h->nmag + 255) / 256, per_sm * sms));
+            // the sweep overlaps the cooperative LLG (MPB_LLG_OVERLAP=0: it
+            // waits for the whole LLG kernel, like every other launch)
+            const char* ov = getenv("MPB_LLG_OVERLAP");
+            g.llg_sync = (ov && atoi(ov) == 0) ? 0 : 1;
         }
     }
     // E-range flags (kSafeBias) let the sweep's H phase skip its division

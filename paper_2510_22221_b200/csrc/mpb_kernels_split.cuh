@@ -524,6 +524,8 @@ __global__ void k_set_run(StepState* st, long long step, const double* src, doub
     st->src_vals = src;
     st->probe_out = probe;
     st->iters_out = iters;
+    st->llg_count = 0;
+    st->llg_stamp = -1;   // no stale stamp can match a step of this run
 }
 
 // Clear a suspension (and the lockstep history) before the host continues

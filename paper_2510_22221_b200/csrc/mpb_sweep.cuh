@@ -270,7 +270,11 @@ k_sweep(Geom g, BufsT<T> b, const mpb_material* __restrict__ mats,
     __shared__ T s_murz[MPB_MAX_MATERIALS];
     unsigned char* ring = smem;
 
-    pdl_wait();   // launched behind the previous step's k_finish (see pdl_wait)
+    // launched behind the previous step's k_finish (see pdl_wait) -- or, with
+    // Geom.llg_sync, behind the cooperative LLG kernel, which itself started
+    // after that k_finish completed: no grid-wide wait then; the CTAs whose
+    // staged H holds magnetic entries wait for the LLG's stamp instead
+    if (!g.llg_sync) pdl_wait();
     if (st->fail) return;
     const int tid = threadIdx.x;
     const int tile = blockIdx.x % sc.tiles;
@@ -308,6 +312,12 @@ k_sweep(Geom g, BufsT<T> b, const mpb_material* __restrict__ mats,
         for (int q = 0; q < kSlots; ++q) mbar_init(&bars[q], 1);
         mbar_fence_init();
     }
+    // Geom.llg_sync: a CTA whose staged planes / entries hold magnetic cells
+    // waits here for the LLG of this step (the barrier below passes the
+    // acquire on to the whole CTA)
+    if (g.llg_sync && tid == NT - 32 && a0 <= sc.mf1 && ah > sc.mf0 && pstart < g.mx1 &&
+        plast >= g.mx0)
+        llg_await_tma(st);
     __syncthreads();
 
     // slot layout: E[3][ecap] | H[3][hcap] | ids[icap]
@@ -744,7 +754,12 @@ __global__ void __launch_bounds__(256, MPB_LLG_MINB) k_llg_pre_coop(
     MagScratch scr, StepState* st) {
     extern __shared__ unsigned long long lhist[];
     __shared__ int lrc[2];
-    if (st->fail) return;
+    pdl_trigger();   // Geom.llg_sync: the sweep's blocks may start now
+    const long long step = st->step;
+    if (st->fail) {
+        if (g.llg_sync && threadIdx.x == 0) llg_publish(st, step);
+        return;
+    }
     CtaLlgStats cs{lhist, lrc};
     cta_stats_init(cs, g.max_iters);
     __syncthreads();
@@ -778,6 +793,10 @@ __global__ void __launch_bounds__(256, MPB_LLG_MINB) k_llg_pre_coop(
     if (lrc[1] > 0) cta_stats_flush(cs, g.max_iters, st);
     cg::this_grid().sync();
     llg_fixup_grid(g, b, mats, ids, cells, ncells, scr, st, mp);
+    if (g.llg_sync) {
+        __syncthreads();
+        if (threadIdx.x == 0) llg_publish(st, step);
+    }
 }
 
 // compact step-n copy of the magnetic cells' H and M from the lattice
