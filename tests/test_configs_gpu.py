@@ -105,6 +105,18 @@ def test_sweep_tile_forms_match_oracle(env, monkeypatch):
     _check("c2", 6)
 
 
+# the LLG launch forms: cooperative LLG overlapped with the sweep (default:
+# only the sweep CTAs staging magnetic H wait for the LLG's step stamp), the
+# cooperative LLG followed by a plain sweep, and two launches (local LLG +
+# fixup) -- same bits
+@pytest.mark.parametrize("env", [{}, {"MPB_LLG_OVERLAP": "0"}, {"MPB_LLG_COOP": "0"}])
+@pytest.mark.parametrize("name,steps", [("c1", 8), ("c3", 4)])
+def test_llg_launch_forms_match_oracle(name, steps, env, monkeypatch):
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    _check(name, steps)
+
+
 def test_nonzero_m_outside_magnets_is_preserved():
     """A resumed state may carry M in non-magnetic cells (the reference never
     touches it there); the library keeps such planes on the host and must hand
