@@ -1211,10 +1211,17 @@ int create_body(const mpb_setup* su, mpb_handle* h, int nranks, int x_lo, int x_
             }
             CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
             h->coop_blocks = std::max(1, std::min((h->nmag + 255) / 256, per_sm * sms));
-            // the sweep overlaps the cooperative LLG (MPB_LLG_OVERLAP=0: it
-            // waits for the whole LLG kernel, like every other launch)
+            // the sweep overlaps the cooperative LLG when the LLG is small:
+            // fp64, at most half of the co-resident blocks (C1 +8-13%, C2
+            // +4%); fp32, at most one block per 16 SMs (C1 +13%) -- the fp32
+            // sweep's three CTAs per SM lose the slots the LLG blocks hold
+            // (C2's 33 blocks: -5%).  A GPU-filling LLG (C3's film, 590K
+            // cells) loses to the early sweep CTAs' competing traffic (fp32
+            // C3 -14%).  MPB_LLG_OVERLAP=0 / 1: never / always
             const char* ov = getenv("MPB_LLG_OVERLAP");
-            g.llg_sync = (ov && atoi(ov) == 0) ? 0 : 1;
+            const int lb = (h->nmag + 255) / 256;
+            g.llg_sync = (h->f32 ? 16 * lb <= sms : 2 * lb <= per_sm * sms) ? 1 : 0;
+            if (ov) g.llg_sync = atoi(ov) != 0 ? 1 : 0;
         }
     }
     // E-range flags (kSafeBias) let the sweep's H phase skip its division

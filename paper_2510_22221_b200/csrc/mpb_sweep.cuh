@@ -754,7 +754,7 @@ __global__ void __launch_bounds__(256, MPB_LLG_MINB) k_llg_pre_coop(
     MagScratch scr, StepState* st) {
     extern __shared__ unsigned long long lhist[];
     __shared__ int lrc[2];
-    pdl_trigger();   // Geom.llg_sync: the sweep's blocks may start now
+    if (g.llg_sync) pdl_trigger();   // the sweep's blocks may start now
     const long long step = st->step;
     if (st->fail) {
         if (g.llg_sync && threadIdx.x == 0) llg_publish(st, step);

@@ -109,7 +109,8 @@ def test_sweep_tile_forms_match_oracle(env, monkeypatch):
 # only the sweep CTAs staging magnetic H wait for the LLG's step stamp), the
 # cooperative LLG followed by a plain sweep, and two launches (local LLG +
 # fixup) -- same bits
-@pytest.mark.parametrize("env", [{}, {"MPB_LLG_OVERLAP": "0"}, {"MPB_LLG_COOP": "0"}])
+@pytest.mark.parametrize("env", [{}, {"MPB_LLG_OVERLAP": "1"}, {"MPB_LLG_OVERLAP": "0"},
+                                 {"MPB_LLG_COOP": "0"}])
 @pytest.mark.parametrize("name,steps", [("c1", 8), ("c3", 4)])
 def test_llg_launch_forms_match_oracle(name, steps, env, monkeypatch):
     for k, v in env.items():
