@@ -154,3 +154,26 @@ def test_guard_free_h_phase_is_bitwise_through_a_run_from_rest(monkeypatch):
         assert np.array_equal(a.lattice.state_arrays()[k], v), k
     for key, v in b.probes.items():
         assert np.array_equal(a.probes[key].samples, v.samples), key
+
+
+def test_concurrent_overlapped_runs_match_oracle():
+    """Four C1 runs at once on one GPU (host threads, one handle + stream
+    each; the C ABI releases the GIL), each with the sweep overlapping its
+    cooperative LLG: CTAs spinning on one handle's step stamp must never
+    hold up another handle's LLG, and every run gives the oracle's bits."""
+    from concurrent.futures import ThreadPoolExecutor
+    cfg, snap, ref, any_mag, start = _case("c1", 8)
+    assert any_mag
+
+    def one(_):
+        return sim.run(cfg, resume={**snap, "fields": {k: v.copy()
+                                                        for k, v in snap["fields"].items()}})
+
+    with ThreadPoolExecutor(4) as ex:
+        results = list(ex.map(one, range(4)))
+    for res in results:
+        for k, v in ref["fields"].items():
+            assert np.array_equal(res.lattice.state_arrays()[k], v), k
+        assert np.array_equal(res.iterations, ref["iterations"])
+        for key, v in ref["probes"].items():
+            assert np.array_equal(res.probes[key].samples, v), key
